@@ -1,0 +1,134 @@
+/*
+ * knnd.h — C ABI of the B200 local-join hot path of comparator K-NN descent
+ * (arXiv 2202.00517; reference package `rankdescent`, pure Python/numpy).
+ *
+ * One shared object, libknnd.so, built for sm_100a.  Every entry point takes
+ * plain device pointers, sizes and a CUDA stream (passed as void*), is
+ * stream-ordered, allocates nothing and keeps no state apart from a per-thread
+ * last-error string and a launch counter.  The caller (the Python host in
+ * paper_2202_00517_b200/, using PyTorch for device buffers) owns all memory.
+ *
+ * Return value: KNND_OK (0) or a negative KNND_E* code; knnd_last_error()
+ * then describes the failure.  Errors never fall back to a CPU path.
+ *
+ * Ids are int32 (n < 2^31, n*K < 2^31).  Tables are row-major.
+ *
+ * The reference interface each entry replaces is cited as file:line relative
+ * to /root/reference/pkg/src/rankdescent/.
+ */
+#ifndef KNND_H
+#define KNND_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KNND_ABI_VERSION 1
+
+enum {
+  KNND_OK = 0,
+  KNND_EINVAL = -1,       /* bad argument (null pointer, size out of range) */
+  KNND_ECUDA = -2,        /* CUDA runtime error (launch / memcpy)           */
+  KNND_EWORKSPACE = -3,   /* workspace smaller than *_workspace_bytes()     */
+  KNND_EUNSUPPORTED = -4, /* K > 64 or other unsupported shape              */
+  KNND_EDEVICE = -5       /* a kernel flagged malformed input (e.g. |U|<K)  */
+};
+
+int knnd_abi_version(void);
+const char *knnd_last_error(void);
+/* Number of kernels this library has launched in this process (all threads). */
+unsigned long long knnd_launch_count(void);
+
+/*
+ * KlRankingSystem.__init__ precompute (similarity.py:87-95):
+ *   log64[i,j] = log(points[i,j])                (fp64, n x d)
+ *   log32[i,j] = (float)log64[i,j], j < d; 0 for d <= j < ld32   (n x ld32)
+ *   xlogx[i]   = sum_j points[i,j] * log64[i,j]  (fp64)
+ * ld32 must be a multiple of 4 and >= d (16-byte aligned rows for float4).
+ */
+int knnd_kl_prepare(const double *points, int64_t n, int32_t d, int32_t ld32,
+                    float *log32, double *log64, double *xlogx, void *stream);
+
+/*
+ * Exact fp64 scores of `ids` against anchor x — the plugin operator
+ * ScoredRankingSystem.batch_scores / KlRankingSystem.batch_scores
+ * (core.py:97-103, similarity.py:101-106):
+ *   out[i] = xlogx[x] - sum_j log64[ids[i], j] * points[x, j]
+ * Each value depends only on (x, ids[i]) (batch independent).
+ */
+int knnd_batch_scores(const double *points, const double *log64, const double *xlogx,
+                      int64_t n, int32_t d, int64_t x, const int32_t *ids, int64_t m,
+                      double *out, void *stream);
+
+/*
+ * Co-friend CSR for the targets owned by this rank — _transpose_csr
+ * (descent.py:151-160), restricted to targets in [row_lo, row_hi):
+ *   cofriends(t) = indices[indptr[t-row_lo] : indptr[t-row_lo+1]]
+ *               = { s : t in friends[s, :] }     (order within a segment is
+ *                                                 unspecified; descent.py
+ *                                                 re-sorts via np.unique)
+ * indptr has (row_hi-row_lo+1) int64 entries, indices has room for n*k.
+ * max_indeg (device int32, may be NULL) receives max segment length.
+ */
+size_t knnd_csr_workspace_bytes(int64_t n, int32_t k, int64_t row_lo, int64_t row_hi);
+int knnd_csr_build(const int32_t *friends, int64_t n, int32_t k, int64_t row_lo,
+                   int64_t row_hi, int64_t *indptr, int32_t *indices, int32_t *max_indeg,
+                   void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * The local join for anchors x in [row_lo, row_hi) — _propose_scored
+ * (descent.py:230-242) as driven by _propose_block / run_round
+ * (descent.py:262-314):
+ *   U_x = unique(F(x) + C(x) + F(F(x)) + F(C(x))) minus {x}
+ *   out_ids[x-row_lo, :] = the K members of U_x with the smallest
+ *                          (score, id), best first, score = batch_scores
+ * with fp64-exact ordering (fp32 screening pass + fp64 rescoring of every
+ * candidate the screening cannot exclude).
+ *   out_kl    (nullable) fp64 scores of out_ids
+ *   out_ucount(nullable) |U_x| per anchor
+ *   tally[0] += sum |U_x|  (RoundStats.comparisons, descent.py:275)
+ *   tally[1] += #rows that differ from friends[x] (order-sensitive,
+ *               RoundStats.changed_friend_sets, descent.py:276-277)
+ *   tally[2] += #anchors with |U_x| < K (malformed input; must stay 0)
+ *   (tally is 4 x uint64, device memory, accumulated — the caller zeroes it)
+ * max_indeg must be >= the longest CSR segment (from knnd_csr_build).
+ */
+size_t knnd_local_join_workspace_bytes(int64_t n, int32_t d, int32_t k, int64_t row_lo,
+                                       int64_t row_hi, int32_t max_indeg);
+int knnd_local_join(const double *points, const float *log32, const double *log64,
+                    const double *xlogx, int64_t n, int32_t d, int32_t ld32,
+                    const int32_t *friends, int32_t k, const int64_t *indptr,
+                    const int32_t *indices, int64_t row_lo, int64_t row_hi,
+                    int32_t max_indeg, int32_t *out_ids, double *out_kl,
+                    int32_t *out_ucount, unsigned long long *tally, void *ws,
+                    size_t ws_bytes, void *stream);
+
+/*
+ * Friend clustering rate count — friend_clustering_rate (descent.py:317-338)
+ * with the sample (xs, i, j) drawn on the host by the reference's own RNG
+ * stream (derive_rng(seed, 3, round), descent.py:330-333, j already shifted):
+ *   *out_count = #{ s : y in F(z) or z in F(y) },  y = F[xs,i], z = F[xs,j]
+ * out_count is overwritten.  rate = count / s_count.
+ */
+int knnd_fcc(const int32_t *friends, int64_t n, int32_t k, const int32_t *xs,
+             const int32_t *is, const int32_t *js, int32_t s_count, int32_t *out_count,
+             void *stream);
+
+/*
+ * Initial row ordering — _sort_rows_by_anchor (descent.py:163-174): each row
+ * of `draws` (rows row_lo..row_hi-1 of the random K-out table) sorted by
+ * (fp64 score, draw position), i.e. a stable argsort on scores.
+ * out_kl (nullable) receives the sorted scores.
+ */
+int knnd_sort_rows(const double *points, const double *log64, const double *xlogx,
+                   int64_t n, int32_t d, int32_t k, int64_t row_lo, int64_t row_hi,
+                   const int32_t *draws, int32_t *out_ids, double *out_kl, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KNND_H */

@@ -1,0 +1,155 @@
+// Shared helpers for the knnd sm_100a kernels: error slot, launch accounting,
+// warp-level (key) sorting networks used by the top-K selections.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/knnd.h"
+
+namespace knnd {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// ---------------------------------------------------------------------------
+// host-side error slot / launch counter (defined in abi.cu)
+void set_error(const char *fmt, ...);
+void count_launch(unsigned n = 1);
+int num_sms();
+
+#define KNND_CHECK_ARG(cond, ...)            \
+  do {                                       \
+    if (!(cond)) {                           \
+      ::knnd::set_error(__VA_ARGS__);        \
+      return KNND_EINVAL;                    \
+    }                                        \
+  } while (0)
+
+#define KNND_CUDA(call)                                                          \
+  do {                                                                           \
+    cudaError_t _e = (call);                                                     \
+    if (_e != cudaSuccess) {                                                     \
+      ::knnd::set_error("%s failed: %s (%s:%d)", #call, cudaGetErrorString(_e), \
+                        __FILE__, __LINE__);                                     \
+      return KNND_ECUDA;                                                         \
+    }                                                                            \
+  } while (0)
+
+#define KNND_LAUNCHED(n)                                                          \
+  do {                                                                            \
+    cudaError_t _e = cudaGetLastError();                                          \
+    if (_e != cudaSuccess) {                                                      \
+      ::knnd::set_error("kernel launch failed: %s (%s:%d)", cudaGetErrorString(_e), \
+                        __FILE__, __LINE__);                                      \
+      return KNND_ECUDA;                                                          \
+    }                                                                             \
+    ::knnd::count_launch(n);                                                      \
+  } while (0)
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// ---------------------------------------------------------------------------
+// keys for the warp sorting networks
+
+// approximate screening key: a float, ascending
+struct KeyF {
+  float v;
+  __device__ __forceinline__ static KeyF inf() { return {__int_as_float(0x7f800000)}; }
+  __device__ __forceinline__ bool lt(const KeyF &o) const { return v < o.v; }
+  __device__ __forceinline__ KeyF shfl(int src) const { return {__shfl_sync(FULL, v, src)}; }
+  __device__ __forceinline__ KeyF shfl_xor(int m) const { return {__shfl_xor_sync(FULL, v, m)}; }
+};
+
+// exact key: (fp64 score, tie id) lexicographic — the ScoredRankingSystem
+// total order (core.py:83-90); for the initial row sort the tie field is the
+// draw position (descent.py:168-169, stable argsort).
+struct KeyD {
+  double s;
+  int id;
+  __device__ __forceinline__ static KeyD inf() { return {__longlong_as_double(0x7ff0000000000000ll), 0x7fffffff}; }
+  __device__ __forceinline__ bool lt(const KeyD &o) const { return s < o.s || (s == o.s && id < o.id); }
+  __device__ __forceinline__ KeyD shfl(int src) const {
+    return {__shfl_sync(FULL, s, src), __shfl_sync(FULL, id, src)};
+  }
+  __device__ __forceinline__ KeyD shfl_xor(int m) const {
+    return {__shfl_xor_sync(FULL, s, m), __shfl_xor_sync(FULL, id, m)};
+  }
+};
+
+template <class Key>
+__device__ __forceinline__ Key kmin(const Key &a, const Key &b) { return b.lt(a) ? b : a; }
+template <class Key>
+__device__ __forceinline__ Key kmax(const Key &a, const Key &b) { return a.lt(b) ? b : a; }
+
+// sort one key per lane ascending across the warp (bitonic, 15 exchanges)
+template <class Key>
+__device__ __forceinline__ Key warp_sort32(Key v, int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      Key o = v.shfl_xor(j);
+      bool up = (lane & k) == 0;
+      bool lower = (lane & j) == 0;
+      v = (lower == up) ? kmin(v, o) : kmax(v, o);
+    }
+  }
+  return v;
+}
+
+// sort a bitonic sequence (one key per lane) ascending (5 exchanges)
+template <class Key>
+__device__ __forceinline__ Key warp_merge32(Key v, int lane) {
+#pragma unroll
+  for (int j = 16; j > 0; j >>= 1) {
+    Key o = v.shfl_xor(j);
+    v = ((lane & j) == 0) ? kmin(v, o) : kmax(v, o);
+  }
+  return v;
+}
+
+// Warp-wide running top-(32*KPL) buffer, element i at lane i%32, register i/32,
+// kept sorted ascending.  Only the first K entries are guaranteed exact (entries
+// between K and 32*KPL may be stale because inserts are filtered by the K-th).
+template <class Key, int KPL>
+struct WarpTopK {
+  Key b[KPL];
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int q = 0; q < KPL; ++q) b[q] = Key::inf();
+  }
+  __device__ __forceinline__ Key get(int i) const {
+    Key r = b[0];
+    if (KPL > 1 && i >= 32) r = b[KPL - 1];
+    return r.shfl(i & 31);
+  }
+  // insert one candidate per lane (pass Key::inf() for "none")
+  __device__ __forceinline__ void insert(Key v, int K, int lane) {
+    Key kth = get(K - 1);
+    bool pass = v.lt(kth);
+    if (!__any_sync(FULL, pass)) return;
+    if (!pass) v = Key::inf();
+    v = warp_sort32(v, lane);
+    Key r = v.shfl(31 - lane);
+    if (KPL == 1) {
+      b[0] = warp_merge32(kmin(b[0], r), lane);
+    } else {
+      Key m = warp_merge32(kmin(b[KPL - 1], r), lane);  // 32 smallest of b1 u v
+      Key r2 = m.shfl(31 - lane);
+      Key lo = kmin(b[0], r2), hi = kmax(b[0], r2);
+      b[0] = warp_merge32(lo, lane);
+      b[KPL - 1] = warp_merge32(hi, lane);
+    }
+  }
+};
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+}  // namespace knnd

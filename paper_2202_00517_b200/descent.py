@@ -1,0 +1,352 @@
+"""K-NN descent on B200 — the drop-in for rankdescent.descent (descent.py:1-391).
+
+Same entry points, arguments, return types and errors as the reference:
+
+  run(dataset, rs, cfg)          -> (friends int64 (n,K) read-only, [RoundStats])
+  run_to_fixed_point(...)        -> same, stops when no row changes
+  run_round(state, rs, cfg)      -> (KnnState, RoundStats)
+  init_random_kout(ds, rs, cfg, rng) -> KnnState
+  friend_clustering_rate(state, S, rng) -> float
+  propose_new_friend_set(x, state, rs)  -> the new row of x
+
+Every random draw is made on the host with the reference's own numpy
+substreams (derive_rng, descent.py:43-45), so inputs and samples are bitwise
+those of the reference; all per-round arithmetic runs in the sm_100a kernels
+of libknnd.so.  The friends table and its co-friend CSR stay resident in HBM
+between rounds; ``KnnState.friends`` downloads lazily.
+
+Under ``torchrun`` (torch.distributed initialised) every rank calls the same
+function; anchors are row-sharded and the table is all-gathered each round
+(see engine.py).  Results do not depend on the rank count.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import time
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from .core import ConfigError, Dataset, ItemId
+from .engine import Csr, Engine
+from .similarity import device_tables_for
+
+_SEED_MASK = 0xFFFFFFFFFFFFFFFF
+
+STREAM_DATA = 1
+STREAM_INIT = 2
+STREAM_FCC = 3
+STREAM_RECALL = 4
+STREAM_WITNESS = 5
+
+
+def derive_rng(seed: int, *path: int) -> np.random.Generator:
+    """descent.py:43-45 — the per-purpose numpy substream."""
+    return np.random.default_rng(np.random.SeedSequence([seed & _SEED_MASK, *path]))
+
+
+def round_budget(n: int, k: int) -> int:
+    """descent.py:48-57 — 2 * ceil(log_k n) with the float guard."""
+    if n < 2 or k < 2:
+        raise ConfigError(f"round budget needs n >= 2 and k >= 2, got n={n}, k={k}")
+    return 2 * math.ceil(math.log(n) / math.log(k) - 1e-9)
+
+
+@dataclass
+class DescentConfig:
+    """descent.py:60-97.  worker_count is accepted for compatibility; on the
+    device it never changes results (nor, here, the schedule)."""
+
+    k: int
+    fcc_sample_count: int = 1000
+    max_rounds: int | None = None
+    seed: int = 0
+    worker_count: int | str = 1
+
+    def __post_init__(self) -> None:
+        if self.k < 2:
+            raise ConfigError(f"k must be >= 2 (the stopping sampler draws friend pairs), got {self.k}")
+        if self.fcc_sample_count < 1:
+            raise ConfigError(f"fcc_sample_count must be >= 1, got {self.fcc_sample_count}")
+        if self.max_rounds is not None and self.max_rounds < 1:
+            raise ConfigError(f"max_rounds must be >= 1, got {self.max_rounds}")
+        if isinstance(self.worker_count, str):
+            if self.worker_count != "auto":
+                raise ConfigError(f'worker_count must be a positive int or "auto", got {self.worker_count!r}')
+        elif self.worker_count < 1:
+            raise ConfigError(f"worker_count must be >= 1, got {self.worker_count}")
+
+    def resolved_max_rounds(self, n: int) -> int:
+        return self.max_rounds if self.max_rounds is not None else round_budget(n, self.k) + 4
+
+    def resolved_workers(self) -> int:
+        return (os.cpu_count() or 1) if self.worker_count == "auto" else int(self.worker_count)
+
+
+@dataclass
+class RoundStats:
+    """descent.py:100-108."""
+
+    round_index: int
+    wall_clock_sec: float
+    fcc: float
+    comparisons: int
+    changed_friend_sets: int
+
+
+def _device(device=None) -> torch.device:
+    if device is not None:
+        dev = torch.device(device)
+    else:
+        if not torch.cuda.is_available():
+            raise RuntimeError("no CUDA device: the B200 descent engine has no CPU fallback")
+        dev = torch.device("cuda", torch.cuda.current_device())
+    if dev.type == "cuda" and dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    return dev
+
+
+class KnnState:
+    """Device-resident snapshot of the friends digraph plus its co-friend CSR
+    (descent.py:111-148).  Constructing one from a host array uploads it and
+    builds the CSR on the GPU; rounds produce new states without host copies.
+    """
+
+    def __init__(self, friends, round_index: int = 0, fcc_history: Sequence[float] = (), *, device=None):
+        arr = np.array(friends, dtype=np.int64)
+        if arr.ndim != 2:
+            raise ValueError(f"friends must be an (n, K) array, got shape {arr.shape}")
+        n, k = arr.shape
+        if arr.size and (arr.min() < 0 or arr.max() >= n):
+            raise ValueError("friends ids must lie in [0, n)")
+        arr.flags.writeable = False
+        eng = Engine(n, k, _device(device))
+        table = eng.upload_table(arr)
+        csr, mx = eng.build_csr(table)
+        self._bind(eng, table, csr, mx, round_index, tuple(fcc_history))
+        self._host = arr
+
+    @classmethod
+    def _from_device(cls, eng: Engine, table, csr: Csr, max_indeg: int, round_index: int, hist) -> "KnnState":
+        st = cls.__new__(cls)
+        st._bind(eng, table, csr, max_indeg, round_index, tuple(hist))
+        return st
+
+    def _bind(self, eng, table, csr, max_indeg, round_index, hist):
+        self._engine = eng
+        self._table = table
+        self._csr = csr
+        self._max_indeg = max_indeg
+        self.round = round_index
+        self.fcc_history = hist
+        self._host = None
+        self._host_csr = None
+
+    # -- reference attributes ----------------------------------------------
+    @property
+    def n(self) -> int:
+        return self._engine.n
+
+    @property
+    def k(self) -> int:
+        return self._engine.k
+
+    @property
+    def device(self) -> torch.device:
+        return self._engine.device
+
+    @property
+    def friends(self) -> np.ndarray:
+        if self._host is None:
+            host = self._table[: self.n].cpu().numpy().astype(np.int64)
+            host.flags.writeable = False
+            self._host = host
+        return self._host
+
+    def _cofriend_csr(self):
+        if self._host_csr is None:
+            s = self._engine.shard
+            if s.world != 1:
+                raise RuntimeError("the host CSR view is only available for single-rank states")
+            ptr = self._csr.indptr.cpu().numpy().astype(np.int64)
+            idx = self._csr.indices[: ptr[-1]].cpu().numpy().astype(np.int64)
+            for t in range(self.n):  # the device leaves segment order unspecified; present it ascending
+                seg = idx[ptr[t]:ptr[t + 1]]
+                seg.sort()
+            self._host_csr = (ptr, idx)
+        return self._host_csr
+
+    @property
+    def cof_indptr(self) -> np.ndarray:
+        return self._cofriend_csr()[0]
+
+    @property
+    def cof_indices(self) -> np.ndarray:
+        return self._cofriend_csr()[1]
+
+    def friends_of(self, x: ItemId) -> np.ndarray:
+        return self.friends[x]
+
+    def cofriends_of(self, x: ItemId) -> np.ndarray:
+        ptr, idx = self._cofriend_csr()
+        return idx[ptr[x]:ptr[x + 1]]
+
+    def friends_dict(self) -> dict[int, set[int]]:
+        return {x: set(map(int, row)) for x, row in enumerate(self.friends)}
+
+    def cofriends_dict(self) -> dict[int, set[int]]:
+        return {x: set(map(int, self.cofriends_of(x))) for x in range(self.n)}
+
+
+# ---------------------------------------------------------------------------
+# host-side draws (the reference's RNG consumption, bit for bit)
+
+
+def random_kout_draws(n: int, k: int, rng: np.random.Generator) -> np.ndarray:
+    """descent.py:193-212 — K distinct uniform non-self targets per row.
+
+    Rejection rows are re-checked only after a redraw (rows without duplicates
+    never change), which consumes the stream exactly as the reference does."""
+    anchors = np.arange(n, dtype=np.int64)[:, None]
+    if n - 1 > 2 * k * k:
+        draws = rng.integers(0, n - 1, size=(n, k), dtype=np.int64)
+        draws += draws >= anchors
+        srt = np.sort(draws, axis=1)
+        bad = np.nonzero((srt[:, 1:] == srt[:, :-1]).any(axis=1))[0]
+        while bad.size:
+            redraw = rng.integers(0, n - 1, size=(bad.size, k), dtype=np.int64)
+            redraw += redraw >= bad[:, None]
+            draws[bad] = redraw
+            srt = np.sort(redraw, axis=1)
+            bad = bad[(srt[:, 1:] == srt[:, :-1]).any(axis=1)]
+        return draws
+    draws = np.empty((n, k), dtype=np.int64)
+    for x in range(n):
+        row = rng.permutation(n - 1)[:k]
+        row += row >= x
+        draws[x] = row
+    return draws
+
+
+def fcc_samples(n: int, k: int, count: int, rng: np.random.Generator) -> np.ndarray:
+    """descent.py:330-333 — (3, count) int32: anchors, slot i, slot j != i."""
+    xs = rng.integers(0, n, size=count)
+    i = rng.integers(0, k, size=count)
+    j = rng.integers(0, k - 1, size=count)
+    j += j >= i
+    return np.stack([xs, i, j]).astype(np.int32)
+
+
+def _to_device(a: np.ndarray, device: torch.device) -> torch.Tensor:
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if device.type == "cuda":
+        t = t.pin_memory()
+    return t.to(device, non_blocking=True)
+
+
+# ---------------------------------------------------------------------------
+# the reference entry points
+
+
+def init_random_kout(dataset: Dataset, rs, cfg: DescentConfig, rng: np.random.Generator, device=None) -> KnnState:
+    """descent.py:177-213 — random K-out digraph, rows ordered by (score, draw position)."""
+    n = len(dataset)
+    k = cfg.k
+    if n <= k:
+        raise ConfigError(f"need n > k, got n={n}, k={k}")
+    tabs = device_tables_for(rs, device)
+    draws = random_kout_draws(n, k, rng)
+    eng = Engine(n, k, tabs.device)
+    table = eng.init_rows(tabs, draws)
+    csr, mx = eng.build_csr(table)
+    return KnnState._from_device(eng, table, csr, mx, 0, ())
+
+
+def _check_state(state: KnnState) -> None:
+    if not isinstance(state, KnnState):
+        raise TypeError(f"expected a paper_2202_00517_b200 KnnState, got {type(state).__name__}")
+
+
+def _round(state: KnnState, tabs, samples_dev, sample_count: int, round_index: int):
+    eng = state._engine
+    nxt, res = eng.round(tabs, state._table, state._csr, state._max_indeg, samples_dev)
+    if res.bad:
+        raise RuntimeError(f"local join saw {res.bad} anchors with fewer than K candidates (malformed table)")
+    rate = res.fcc_count / sample_count
+    new_state = KnnState._from_device(eng, nxt, res.csr, res.max_indeg, round_index, state.fcc_history + (rate,))
+    return new_state, res, rate
+
+
+def run_round(state: KnnState, rs, cfg: DescentConfig) -> tuple[KnnState, RoundStats]:
+    """descent.py:282-314 — one synchronous round against the snapshot."""
+    _check_state(state)
+    t0 = time.perf_counter()
+    tabs = device_tables_for(rs, state.device)
+    r = state.round + 1
+    smp = fcc_samples(state.n, state.k, cfg.fcc_sample_count, derive_rng(cfg.seed, STREAM_FCC, r))
+    new_state, res, rate = _round(state, tabs, _to_device(smp, state.device), cfg.fcc_sample_count, r)
+    stats = RoundStats(r, time.perf_counter() - t0, rate, res.comparisons, res.changed)
+    return new_state, stats
+
+
+def friend_clustering_rate(state: KnnState, sample_count: int, rng: np.random.Generator) -> float:
+    """descent.py:317-338 — sampled friend clustering rate, counted on the GPU."""
+    _check_state(state)
+    if state.k < 2:
+        raise ConfigError(f"friend clustering rate needs k >= 2, got {state.k}")
+    if sample_count < 1:
+        raise ConfigError(f"sample_count must be >= 1, got {sample_count}")
+    smp = fcc_samples(state.n, state.k, sample_count, rng)
+    cnt = state._engine.fcc(state._table, _to_device(smp, state.device))
+    return cnt / sample_count
+
+
+def propose_new_friend_set(x: ItemId, state: KnnState, rs) -> np.ndarray:
+    """descent.py:252-259 — the K best of x's friends and candidates, best first."""
+    _check_state(state)
+    eng = state._engine
+    s = eng.shard
+    if not (s.lo <= x < s.hi):
+        raise ValueError(f"anchor {x} is not owned by this rank")
+    tabs = device_tables_for(rs, state.device)
+    sub = Csr(state._csr.indptr[x - s.lo:], state._csr.indices, x, x + 1)
+    out = torch.empty((1, state.k), dtype=torch.int32, device=state.device)
+    tally = torch.zeros(4, dtype=torch.int64, device=state.device)
+    eng.ops.join(tabs, state._table, state.n, state.k, sub, state._max_indeg, out, tally)
+    return out[0].cpu().numpy().astype(np.int64)
+
+
+def _run_rounds(dataset: Dataset, rs, cfg: DescentConfig, max_rounds: int, stop_on_fixed_point: bool):
+    n = len(dataset)
+    state = init_random_kout(dataset, rs, cfg, derive_rng(cfg.seed, STREAM_INIT))
+    tabs = device_tables_for(rs, state.device)
+    # every round's FCC sample is a function of (seed, round) only: draw them all up front
+    smp = np.stack([fcc_samples(n, cfg.k, cfg.fcc_sample_count, derive_rng(cfg.seed, STREAM_FCC, r))
+                    for r in range(1, max_rounds + 1)])
+    smp_dev = _to_device(smp, state.device)
+    history: list[RoundStats] = []
+    for r in range(1, max_rounds + 1):
+        t0 = time.perf_counter()
+        state, res, rate = _round(state, tabs, smp_dev[r - 1], cfg.fcc_sample_count, r)
+        history.append(RoundStats(r, time.perf_counter() - t0, rate, res.comparisons, res.changed))
+        if stop_on_fixed_point:
+            if res.changed == 0:
+                break
+        elif len(history) >= 2 and history[-1].fcc <= history[-2].fcc:
+            break
+    return state.friends, history
+
+
+def run(dataset: Dataset, rs, cfg: DescentConfig) -> tuple[np.ndarray, list[RoundStats]]:
+    """descent.py:365-373 — init, then rounds until the clustering rate stalls."""
+    return _run_rounds(dataset, rs, cfg, cfg.resolved_max_rounds(len(dataset)), stop_on_fixed_point=False)
+
+
+def run_to_fixed_point(dataset: Dataset, rs, cfg: DescentConfig) -> tuple[np.ndarray, list[RoundStats]]:
+    """descent.py:376-391 — rounds until no row changes (cap 8*budget+16)."""
+    cap = cfg.max_rounds if cfg.max_rounds is not None else 8 * round_budget(len(dataset), cfg.k) + 16
+    return _run_rounds(dataset, rs, cfg, cap, stop_on_fixed_point=True)

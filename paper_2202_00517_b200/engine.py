@@ -1,0 +1,223 @@
+"""Device round engine: row shards, the per-round kernel sequence, and the
+table exchange between ranks.
+
+One process per GPU.  Rank r of P owns anchors [r*chunk, min((r+1)*chunk, n))
+with chunk = ceil(n/P); every rank holds the full vector tables and the full
+int32 friends table (padded to P*chunk rows so the NCCL all-gather is
+in-place and equal-sized).  A round (run_round, descent.py:282-314) is:
+
+  local join (own anchors -> own slice of the next table)     knnd_local_join
+  all-gather of the next table, all-reduce of the tallies      NCCL (P > 1)
+  co-friend CSR of the next table for own targets              knnd_csr_build
+  FCC count of the next table (replicated on every rank)       knnd_fcc
+  one small device->host read: tallies, FCC count, max in-degree
+
+The kernel calls go through an ``ops`` object; ``CudaOps`` is the product
+(libknnd.so).  Tests inject a CPU stand-in to exercise the multi-rank logic
+under the gloo backend without a GPU.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+
+
+@dataclass(frozen=True)
+class Shard:
+    rank: int
+    world: int
+    n: int
+
+    @property
+    def chunk(self) -> int:
+        return -(-self.n // self.world)
+
+    @property
+    def lo(self) -> int:
+        return min(self.rank * self.chunk, self.n)
+
+    @property
+    def hi(self) -> int:
+        return min(self.lo + self.chunk, self.n)
+
+    @property
+    def padded_rows(self) -> int:
+        return self.chunk * self.world
+
+
+@dataclass
+class Csr:
+    indptr: torch.Tensor  # int64 (hi-lo+1,)
+    indices: torch.Tensor  # int32 (n*K,)
+    lo: int
+    hi: int
+
+
+class CudaOps:
+    """The product kernel calls (libknnd.so) on one device's current stream."""
+
+    def __init__(self, device: torch.device):
+        self.device = device
+        self._ws = {}
+
+    def _stream(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def _workspace(self, key: str, nbytes: int) -> torch.Tensor:
+        buf = self._ws.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+            self._ws[key] = buf
+        return buf
+
+    def csr(self, table: torch.Tensor, n: int, k: int, lo: int, hi: int, max_out: torch.Tensor | None) -> Csr:
+        indptr = torch.empty(hi - lo + 1, dtype=torch.int64, device=self.device)
+        indices = torch.empty(max(n * k, 1), dtype=torch.int32, device=self.device)
+        nbytes = _lib.load().knnd_csr_workspace_bytes(n, k, lo, hi)
+        ws = self._workspace("csr", nbytes)
+        _lib.call("knnd_csr_build", table.data_ptr(), n, k, lo, hi, indptr.data_ptr(), indices.data_ptr(),
+                  max_out.data_ptr() if max_out is not None else None, ws.data_ptr(), ws.numel(), self._stream())
+        return Csr(indptr, indices, lo, hi)
+
+    def join(self, tabs, table: torch.Tensor, n: int, k: int, csr: Csr, max_indeg: int, out_rows: torch.Tensor,
+             tally: torch.Tensor, out_kl: torch.Tensor | None = None, out_ucount: torch.Tensor | None = None) -> None:
+        nbytes = _lib.load().knnd_local_join_workspace_bytes(n, tabs.d, k, csr.lo, csr.hi, max_indeg)
+        ws = self._workspace("join", nbytes)
+        _lib.call("knnd_local_join", tabs.points.data_ptr(), tabs.log32.data_ptr(), tabs.log64.data_ptr(),
+                  tabs.xlogx.data_ptr(), n, tabs.d, tabs.ld, table.data_ptr(), k, csr.indptr.data_ptr(),
+                  csr.indices.data_ptr(), csr.lo, csr.hi, max_indeg, out_rows.data_ptr(),
+                  out_kl.data_ptr() if out_kl is not None else None,
+                  out_ucount.data_ptr() if out_ucount is not None else None, tally.data_ptr(), ws.data_ptr(),
+                  ws.numel(), self._stream())
+
+    def fcc(self, table: torch.Tensor, n: int, k: int, samples: torch.Tensor, out_count: torch.Tensor) -> None:
+        s = samples.shape[1]
+        _lib.call("knnd_fcc", table.data_ptr(), n, k, samples[0].data_ptr(), samples[1].data_ptr(),
+                  samples[2].data_ptr(), s, out_count.data_ptr(), self._stream())
+
+    def sort_rows(self, tabs, rows: torch.Tensor, k: int, lo: int, hi: int, out_kl: torch.Tensor | None = None):
+        # in place: each warp reads its row before writing it back
+        _lib.call("knnd_sort_rows", tabs.points.data_ptr(), tabs.log64.data_ptr(), tabs.xlogx.data_ptr(), tabs.n,
+                  tabs.d, k, lo, hi, rows.data_ptr(), rows.data_ptr(),
+                  out_kl.data_ptr() if out_kl is not None else None, self._stream())
+
+
+@dataclass
+class RoundResult:
+    csr: Csr
+    comparisons: int
+    changed: int
+    bad: int
+    fcc_count: int
+    max_indeg: int
+
+
+class Engine:
+    """Shard-aware round engine for one device (and one rank)."""
+
+    def __init__(self, n: int, k: int, device: torch.device, group=None, ops=None):
+        self.n, self.k = n, k
+        self.device = device
+        self.group = group
+        if dist.is_available() and dist.is_initialized():
+            rank, world = dist.get_rank(group), dist.get_world_size(group)
+        else:
+            rank, world = 0, 1
+        self.shard = Shard(rank, world, n)
+        self.ops = ops if ops is not None else CudaOps(device)
+        # int64 slots: [0:4] tally (comparisons, changed, bad, -), [4] = int32 (fcc count, max in-degree),
+        # [5] this rank's comparisons
+        self.stats = torch.zeros(8, dtype=torch.int64, device=device)
+        self._stats32 = self.stats.view(torch.int32)
+        # optional CUDA-event bracketing of each local join (bench.py roofline)
+        self.join_events: list | None = None
+
+    # -- tables -----------------------------------------------------------
+    def alloc_table(self) -> torch.Tensor:
+        return torch.empty((self.shard.padded_rows, self.k), dtype=torch.int32, device=self.device)
+
+    def own_rows(self, table: torch.Tensor) -> torch.Tensor:
+        s = self.shard
+        return table[s.lo:s.hi]
+
+    def exchange(self, table: torch.Tensor) -> None:
+        """In-place all-gather of every rank's slice (NCCL over NVLink)."""
+        s = self.shard
+        if s.world == 1:
+            return
+        flat = table.view(-1)
+        mine = flat[s.rank * s.chunk * self.k:(s.rank + 1) * s.chunk * self.k]
+        if dist.get_backend(self.group) != "nccl":
+            mine = mine.clone()  # NCCL gathers in place; other backends want a separate input
+        dist.all_gather_into_tensor(flat, mine, group=self.group)
+
+    def upload_rows(self, host_rows: np.ndarray, table: torch.Tensor) -> int:
+        """Copy this rank's rows of a host (n, K) table into `table`; returns bytes copied."""
+        s = self.shard
+        src = torch.from_numpy(np.ascontiguousarray(host_rows[s.lo:s.hi], dtype=np.int32))
+        if self.device.type == "cuda":
+            src = src.pin_memory()
+        self.own_rows(table).copy_(src, non_blocking=True)
+        return src.numel() * 4
+
+    def upload_table(self, host: np.ndarray) -> torch.Tensor:
+        """A full host table onto the device (every rank uploads all rows)."""
+        t = self.alloc_table()
+        src = torch.from_numpy(np.ascontiguousarray(host, dtype=np.int32))
+        if self.device.type == "cuda":
+            src = src.pin_memory()
+        t[: self.n].copy_(src, non_blocking=True)
+        return t
+
+    # -- kernels ----------------------------------------------------------
+    def build_csr(self, table: torch.Tensor) -> tuple[Csr, int]:
+        s = self.shard
+        mx = self._stats32[9:10]
+        csr = self.ops.csr(table, self.n, self.k, s.lo, s.hi, mx)
+        return csr, int(mx.item())
+
+    def init_rows(self, tabs, draws: np.ndarray) -> torch.Tensor:
+        """_sort_rows_by_anchor (descent.py:163-174) for own rows, then exchange."""
+        s = self.shard
+        table = self.alloc_table()
+        self.upload_rows(draws, table)
+        self.ops.sort_rows(tabs, self.own_rows(table), self.k, s.lo, s.hi)
+        self.exchange(table)
+        return table
+
+    def round(self, tabs, table: torch.Tensor, csr: Csr, max_indeg: int, samples: torch.Tensor | None,
+              out_kl: torch.Tensor | None = None, out_ucount: torch.Tensor | None = None
+              ) -> tuple[torch.Tensor, RoundResult]:
+        tally = self.stats[0:4]
+        tally.zero_()
+        nxt = self.alloc_table()
+        ev = None
+        if self.join_events is not None:
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record()
+        self.ops.join(tabs, table, self.n, self.k, csr, max_indeg, self.own_rows(nxt), tally, out_kl, out_ucount)
+        if ev is not None:
+            ev[1].record()
+        self.stats[5:6].copy_(tally[0:1])  # this rank's comparisons (before the all-reduce)
+        if self.shard.world > 1:
+            self.exchange(nxt)
+            dist.all_reduce(tally, group=self.group)
+        s = self.shard
+        csr_next = self.ops.csr(nxt, self.n, self.k, s.lo, s.hi, self._stats32[9:10])
+        if samples is not None:
+            self.ops.fcc(nxt, self.n, self.k, samples, self._stats32[8:9])
+        host = self.stats.cpu()  # the one synchronisation of the round
+        h32 = host.view(torch.int32)
+        if ev is not None:
+            self.join_events.append((ev[0].elapsed_time(ev[1]), int(host[5])))
+        return nxt, RoundResult(csr_next, int(host[0]), int(host[1]), int(host[2]), int(h32[8]), int(h32[9]))
+
+    def fcc(self, table: torch.Tensor, samples: torch.Tensor) -> int:
+        self.ops.fcc(table, self.n, self.k, samples, self._stats32[8:9])
+        return int(self._stats32[8].item())

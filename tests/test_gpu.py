@@ -1,0 +1,276 @@
+"""GPU parity tests: the libknnd.so kernels against the oracle and the
+reference's golden vectors.  Run on a B200: ``pytest -m gpu``."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2202_00517_b200 as b2
+from oracle import native, port
+from parity import KL_REL, sha_i32, tie_aware_diff
+from paper_2202_00517_b200.engine import Engine
+
+pytestmark = pytest.mark.gpu
+
+SMALL = [
+    "n300_d6_k7_s3", "n500_d5_k6_s23", "n2000_d6_k8_s20", "n1000_d20_k20_s1", "n1500_d16_k10_s7",
+    "n600_d50_k30_s2", "n800_d10_k40_s5", "n5_d3_k4_s22", "n12_d3_k6_s4", "n4000_d5_k10_s0",
+]
+
+
+def _points(meta):
+    return port.experiment_points(meta["n"], meta["d"], meta["seed"])
+
+
+# ---------------------------------------------------------------------------
+# operator pins
+
+
+def test_library_is_native_and_counts_launches(cuda):
+    before = b2.launch_count()
+    rs = b2.KlRankingSystem(np.array([[0.5, 0.5], [0.25, 0.75], [0.1, 0.9]]))
+    rs.batch_scores(0, np.array([1, 2]))
+    assert b2.launch_count() >= before + 2  # kl_prepare + batch_scores
+
+
+def test_known_kl_values(cuda, known):
+    rs = b2.KlRankingSystem(np.array(known["kl_points"]))
+    assert rs.score(0, 1) == pytest.approx(known["kl_01"], rel=1e-12)
+    assert rs.score(0, 2) == pytest.approx(known["kl_02"], rel=1e-12)
+    assert rs.score(1, 0) == pytest.approx(known["kl_10"], rel=1e-12)
+    assert rs.compare(0, 1, 2) < 0 and rs.compare(0, 2, 1) > 0
+
+
+def test_batch_scores_pins_and_batch_independence(cuda, known):
+    pts = b2.sample_simplex_uniform(10, 300, 8)
+    rs = b2.KlRankingSystem(pts)
+    for x, ref in known["batch_scores"].items():
+        full = rs.batch_scores(int(x))
+        np.testing.assert_allclose(full, np.array(ref), rtol=1e-12, atol=1e-14)  # D(x||x) ~ 0
+        ids = np.random.default_rng(0).choice(300, size=50, replace=False)
+        assert np.array_equal(rs.batch_scores(int(x), ids), full[ids])
+
+
+# ---------------------------------------------------------------------------
+# K1 co-friend CSR
+
+
+@pytest.mark.parametrize("n,k,lo,hi", [(1000, 7, 0, 1000), (5000, 20, 1200, 3700), (64, 3, 0, 64), (9000, 30, 0, 1)])
+def test_csr_matches_transpose(cuda, n, k, lo, hi):
+    rng = np.random.default_rng(n + k)
+    table = b2.random_kout_draws(n, k, rng)
+    ptr, idx = native.transpose(table)
+    eng = Engine(n, k, cuda)
+    t = eng.upload_table(table)
+    csr = eng.ops.csr(t, n, k, lo, hi, eng._stats32[9:10])
+    got_ptr = csr.indptr.cpu().numpy()
+    exp_ptr = ptr[lo:hi + 1] - ptr[lo]
+    assert np.array_equal(got_ptr, exp_ptr)
+    got_idx = csr.indices.cpu().numpy()
+    for t_ in range(lo, hi):
+        a = np.sort(got_idx[got_ptr[t_ - lo]:got_ptr[t_ - lo + 1]])
+        b = idx[ptr[t_]:ptr[t_ + 1]]
+        assert np.array_equal(a, b), t_
+    assert int(eng._stats32[9].item()) == int(np.diff(ptr[lo:hi + 1]).max())
+
+
+# ---------------------------------------------------------------------------
+# K6 initial rows and the whole init
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_init_matches_reference(cuda, small_meta, small_tables, name):
+    meta = small_meta[name]
+    pts = _points(meta)
+    rs = b2.KlRankingSystem(pts, validate=False)
+    cfg = b2.DescentConfig(k=meta["k"], seed=meta["seed"])
+    st = b2.init_random_kout(b2.Dataset(pts), rs, cfg, b2.derive_rng(meta["seed"], 2))
+    assert sha_i32(st.friends) == meta["init_sha"]
+    assert np.array_equal(st.friends, small_tables[f"{name}/init"])
+
+
+# ---------------------------------------------------------------------------
+# K2-K4 local join, same input
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_round1_same_input_exact(cuda, small_meta, small_tables, name):
+    meta = small_meta[name]
+    pts = _points(meta)
+    rs = b2.KlRankingSystem(pts, validate=False)
+    cfg = b2.DescentConfig(k=meta["k"], seed=meta["seed"])
+    st = b2.KnnState(small_tables[f"{name}/init"])
+    nxt, stats = b2.run_round(st, rs, cfg)
+    r1 = meta["rounds"][0]
+    assert stats.comparisons == r1["comparisons"]
+    assert stats.changed_friend_sets == r1["changed"]
+    assert round(stats.fcc * cfg.fcc_sample_count) == r1["fcc_count"]
+    got = nxt.friends
+    if sha_i32(got) != r1["sha"]:
+        diff = tie_aware_diff(native.Tables(pts), small_tables[f"{name}/round1"], got)
+        assert not diff["violations"], diff
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_full_run_trajectory(cuda, small_meta, small_tables, name):
+    meta = small_meta[name]
+    pts = _points(meta)
+    rs = b2.KlRankingSystem(pts, validate=False)
+    cfg = b2.DescentConfig(k=meta["k"], seed=meta["seed"])
+    final, hist = b2.run(b2.Dataset(pts), rs, cfg)
+    assert final.dtype == np.int64 and not final.flags.writeable
+    assert len(hist) == len(meta["rounds"])
+    for h, r in zip(hist, meta["rounds"]):
+        assert (h.round_index, h.comparisons, h.changed_friend_sets) == (r["round"], r["comparisons"], r["changed"])
+        assert h.fcc == r["fcc"]
+    assert sha_i32(final) == meta["rounds"][-1]["sha"]
+
+
+def test_ucount_and_kl_values_vs_oracle(cuda, small_meta, small_tables):
+    name = "n1000_d20_k20_s1"
+    meta = small_meta[name]
+    pts = _points(meta)
+    n, k = meta["n"], meta["k"]
+    rs = b2.KlRankingSystem(pts, validate=False)
+    tabs = rs.device_tables()
+    init = small_tables[f"{name}/init"]
+    st = b2.KnnState(init)
+    out = torch.empty((n, k), dtype=torch.int32, device=cuda)
+    kl = torch.empty((n, k), dtype=torch.float64, device=cuda)
+    uc = torch.empty(n, dtype=torch.int32, device=cuda)
+    tally = torch.zeros(4, dtype=torch.int64, device=cuda)
+    st._engine.ops.join(tabs, st._table, n, k, st._csr, st._max_indeg, out, tally, kl, uc)
+    o_rows, o_kl, o_uc, o_comp, o_changed = native.local_join(native.Tables(pts), init)
+    assert np.array_equal(uc.cpu().numpy(), o_uc)
+    assert np.array_equal(out.cpu().numpy(), o_rows)
+    np.testing.assert_allclose(kl.cpu().numpy(), o_kl, rtol=KL_REL, atol=0)
+    np.testing.assert_allclose(kl.cpu().numpy(), o_kl, rtol=1e-12, atol=1e-15)
+    assert tally.cpu().tolist()[:3] == [o_comp, o_changed, 0]
+
+
+def _hub_table(n, k, hubs, rng):
+    """Random K-out table where `hubs[i]` receives about counts[i] extra arcs."""
+    t = b2.random_kout_draws(n, k, rng)
+    for hub, cnt in hubs:
+        rows = rng.choice(np.setdiff1d(np.arange(n), [hub]), size=cnt, replace=False)
+        for r in rows:
+            if hub not in t[r]:
+                t[r, rng.integers(0, k)] = hub
+    return t
+
+
+@pytest.mark.parametrize("n,d,k", [(20000, 5, 10), (30000, 20, 20), (12000, 50, 30), (6000, 8, 64)])
+def test_size_classes_and_hubs_vs_oracle(cuda, n, d, k):
+    """Anchors spread over all three size classes (warp-block smem, large smem,
+    global-table hubs) give exactly the oracle's rows and |U|."""
+    rng = np.random.default_rng(n + d + k)
+    pts = port.experiment_points(n, d, 3)
+    hubs = [(7, n // 4), (11, n // 10), (13, 40 * k), (17, 8 * k), (19, 3 * k), (23, 2 * k)]
+    table = _hub_table(n, k, hubs, rng)
+    table = native.sort_rows(native.Tables(pts), table)
+    rs = b2.KlRankingSystem(pts, validate=False)
+    st = b2.KnnState(table)
+    tabs = rs.device_tables()
+    out = torch.empty((n, k), dtype=torch.int32, device=cuda)
+    uc = torch.empty(n, dtype=torch.int32, device=cuda)
+    tally = torch.zeros(4, dtype=torch.int64, device=cuda)
+    st._engine.ops.join(tabs, st._table, n, k, st._csr, st._max_indeg, out, tally, None, uc)
+    o_rows, _, o_uc, o_comp, o_changed = native.local_join(native.Tables(pts), table)
+    assert np.array_equal(uc.cpu().numpy(), o_uc)
+    got = out.cpu().numpy()
+    if not np.array_equal(got, o_rows):
+        diff = tie_aware_diff(native.Tables(pts), o_rows, got)
+        assert not diff["violations"], diff
+    assert tally.cpu().tolist()[:3] == [o_comp, o_changed, 0]
+
+
+# ---------------------------------------------------------------------------
+# FCC
+
+
+def test_fcc_extremes(cuda, known):
+    full = b2.KnnState(np.array([[1, 2], [0, 2], [0, 1]]))
+    assert b2.friend_clustering_rate(full, 500, b2.derive_rng(0, 3, 1)) == known["fcc_complete"] == 1.0
+    bip = b2.KnnState(np.array([[2, 3], [2, 3], [0, 1], [0, 1]]))
+    assert b2.friend_clustering_rate(bip, 500, b2.derive_rng(1, 3, 1)) == known["fcc_bipartite"] == 0.0
+
+
+def test_fcc_matches_oracle_on_random_table(cuda):
+    n, k = 5000, 12
+    t = b2.random_kout_draws(n, k, np.random.default_rng(5))
+    st = b2.KnnState(t)
+    for r in range(1, 4):
+        rate = b2.friend_clustering_rate(st, 3000, b2.derive_rng(9, 3, r))
+        cnt, ref = port.fcc_rate(t, 3000, 9, r)
+        assert rate == ref
+
+
+def test_cofriend_view_matches_transpose(cuda):
+    t = b2.random_kout_draws(300, 5, np.random.default_rng(2))
+    st = b2.KnnState(t)
+    ptr, idx = port.cofriend_csr(t)
+    assert np.array_equal(st.cof_indptr, ptr)
+    assert np.array_equal(st.cof_indices, idx)
+
+
+def test_propose_new_friend_set(cuda, small_meta, small_tables):
+    name = "n300_d6_k7_s3"
+    meta = small_meta[name]
+    pts = _points(meta)
+    rs = b2.KlRankingSystem(pts, validate=False)
+    st = b2.KnnState(small_tables[f"{name}/init"])
+    r1 = small_tables[f"{name}/round1"]
+    for x in range(0, 300, 13):
+        assert np.array_equal(b2.propose_new_friend_set(x, st, rs), r1[x])
+
+
+# ---------------------------------------------------------------------------
+# BASELINE configs against the reference's recorded trajectories
+
+
+def _trajectory_check(traj, name, tie_check_threads=0):
+    ref = traj[name]
+    n, d, k, seed = ref["n"], ref["d"], ref["k"], ref["seed"]
+    pts = port.experiment_points(n, d, seed)
+    rs = b2.KlRankingSystem(pts, validate=False)
+    cfg = b2.DescentConfig(k=k, seed=seed)
+    st = b2.init_random_kout(b2.Dataset(pts), rs, cfg, b2.derive_rng(seed, 2))
+    assert sha_i32(st.friends) == ref["init_sha"]
+    tab = None
+    hist = []
+    for r in ref["rounds"]:
+        prev = st
+        st, stats = b2.run_round(st, rs, cfg)
+        hist.append(stats)
+        got = st.friends
+        if sha_i32(got) != r["sha"]:
+            # not bit-identical: every difference must be an fp64 tie (same input)
+            tab = tab or native.Tables(pts)
+            o_rows, _, _, o_comp, _ = native.local_join(tab, prev.friends, threads=tie_check_threads)
+            diff = tie_aware_diff(tab, o_rows, got)
+            assert not diff["violations"], (r["round"], diff)
+            assert stats.comparisons == o_comp
+        else:
+            assert stats.comparisons == r["comparisons"]
+            assert stats.changed_friend_sets == r["changed"]
+        assert round(stats.fcc * 1000) == r["fcc_count"]
+        if len(hist) >= 2 and hist[-1].fcc <= hist[-2].fcc:
+            break
+    assert len(hist) == len(ref["rounds"])
+
+
+def test_c1_trajectory(cuda, trajectories):
+    _trajectory_check(trajectories, "c1")
+
+
+def test_c2_trajectory(cuda, trajectories):
+    _trajectory_check(trajectories, "c2")
+
+
+@pytest.mark.slow
+def test_c3_trajectory(cuda, trajectories):
+    if "c3" not in trajectories or "rounds_used" not in trajectories["c3"]:
+        pytest.skip("reference C3 trajectory not recorded yet")
+    _trajectory_check(trajectories, "c3")
