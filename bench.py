@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""bench.py — KL comparisons/s + time-to-termination of K-NN descent on B200.
+
+Workload (BASELINE.json metric, configs[2] = C3): n = 1,000,000 points of the
+20-dim simplex (flat Dirichlet, seed 0, the reference's bench.generate_points
+stream), K = 20, KL comparator, seeded random K-out initial digraph, FCC
+termination.  One *step* = one complete descent on the device from the
+resident unsorted initial draws: initial row sort, then rounds (local join,
+table exchange, co-friend CSR, FCC) until the clustering rate stalls — the
+reference's timed region (bench.py:155-157) minus the host RNG draws, which
+are input generation here and are timed in `e2e`.
+
+  value      total comparisons of the step / device time of the step (CUDA
+             events, max over ranks), summed over the K timed steps
+  e2e        the same metric through the public API paper_2202_00517_b200.run
+             from HOST points: points upload, device tables, host RNG init
+             draws + upload, the rounds, and the final table download
+  roofline   the local-join launch (the dominant kernel): algorithmic bytes
+             4*d per comparison (the fp32 log row of each unique candidate)
+             / its CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline  the C oracle (oracle/knnd_oracle.c, all host threads) on a
+             bounded sample of the same workload: the round-1 local join of
+             200,000 sampled anchors
+
+`--impl reference` times that CPU implementation alone (rank 0 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "KL comparisons/sec + time-to-termination, n=1M d=20 K=20, at 1/2/4/8 B200"
+UNIT = "comparisons/s"
+CONFIGS = {
+    "c1": (10_000, 5, 10),
+    "c2": (100_000, 10, 20),
+    "c3": (1_000_000, 20, 20),
+    "c4": (1_000_000, 50, 30),
+    "c5": (10_000_000, 20, 20),
+}
+CPU_SAMPLE_ANCHORS = 200_000
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--seed", type=int, default=0)
+    return ap.parse_args()
+
+
+def workload_desc(cfg, n, d, k):
+    return (f"{cfg.upper()}: n={n} d={d} K={k} KL, full descent to FCC termination from the seeded "
+            "random K-out draws (resident in HBM)")
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+
+
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int, enabled: bool = True):
+        self.proc = None
+        self.index = index
+        if enabled:
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                     "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            except OSError:
+                self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU side: the C oracle on a bounded sample (checker code, never the product)
+
+
+def cpu_sample_setup(n, d, k, seed, anchors=CPU_SAMPLE_ANCHORS):
+    from oracle import native, port
+
+    pts = port.experiment_points(n, d, seed)
+    tab = native.Tables(pts)
+    init = native.sort_rows(tab, port.random_kout_draws(n, k, port.substream(seed, port.TAG_INIT)))
+    csr = native.transpose(init)
+    sample = np.sort(np.random.default_rng(seed).choice(n, size=min(anchors, n), replace=False))
+    return tab, init, csr, sample
+
+
+def cpu_sample_run(tab, init, csr, sample):
+    from oracle import native
+
+    t0 = time.perf_counter()
+    _, _, _, comps, _ = native.local_join(tab, init, sample, csr=csr)
+    return comps, time.perf_counter() - t0
+
+
+def cpu_threads():
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n, d, k = CONFIGS[args.config]
+    tab, init, csr, sample = cpu_sample_setup(n, d, k, args.seed)
+    for _ in range(args.warmup):
+        cpu_sample_run(tab, init, csr, sample)
+    comps = secs = 0.0
+    for _ in range(args.steps):
+        c, s = cpu_sample_run(tab, init, csr, sample)
+        comps += c
+        secs += s
+    v = comps / secs
+    cores = cpu_threads()
+    sample_desc = (f"round-1 local join (descent.py:230-242) of {sample.size} uniformly sampled anchors of "
+                   f"{args.config.upper()} via the C oracle, {cores} OpenMP threads")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_desc(args.config, n, d, k) + " [CPU: bounded anchor sample]",
+                   "n": n, "d": d, "k": k, "seed": args.seed, "parallelism": "host threads"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample_desc},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# the B200 arm
+
+
+def b200_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2202_00517_b200 as b2
+    from paper_2202_00517_b200.descent import _to_device, descend_resident, draw_fcc_schedule
+    from paper_2202_00517_b200.engine import Engine
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    n, d, k = CONFIGS[args.config]
+    seed = args.seed
+    cfg = b2.DescentConfig(k=k, seed=seed)
+    max_rounds = cfg.resolved_max_rounds(n)
+
+    # ---- inputs (host generation is not timed in `value`)
+    pts = b2.sample_simplex_uniform(d, n, b2.derive_rng(seed, b2.STREAM_DATA, d))
+    rs = b2.KlRankingSystem(pts, validate=False)
+    tabs = rs.device_tables(dev)
+    draws = b2.random_kout_draws(n, k, b2.derive_rng(seed, b2.STREAM_INIT))
+    eng = Engine(n, k, dev)
+    draws_dev = eng.alloc_table()
+    eng.upload_rows(draws, draws_dev)
+    smp_dev = _to_device(draw_fcc_schedule(n, k, cfg, max_rounds), dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+
+    def step(profile: bool):
+        table = draws_dev.clone()
+        eng.join_events = [] if profile else None
+        state, hist = descend_resident(eng, tabs, table, smp_dev, cfg.fcc_sample_count, max_rounds)
+        ev = eng.join_events or []
+        eng.join_events = None
+        return hist, ev
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step(False)
+    torch.cuda.synchronize()
+
+    clocks = Clocks(local, enabled=not args.no_clocks)
+    step_ms, comps, rounds, join_ms, join_comps = [], 0, [], 0.0, 0
+    launches0 = b2.launch_count()
+    for _ in range(args.steps):
+        flush.zero_()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        hist, ev = step(True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        step_ms.append(e0.elapsed_time(e1))
+        comps += sum(h.comparisons for h in hist)
+        rounds.append(len(hist))
+        join_ms += sum(m for m, _ in ev)
+        join_comps += sum(c for _, c in ev)
+    launches = b2.launch_count() - launches0
+    clk = clocks.stop()
+
+    t = torch.tensor(step_ms + [float(launches)], dtype=torch.float64, device=dev)
+    if world > 1:
+        tl = t.clone()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tl, op=dist.ReduceOp.SUM)
+        launches_total = int(tl[-1].item())
+    else:
+        launches_total = launches
+    step_ms = t[:-1].tolist()
+    total_s = sum(step_ms) / 1e3
+    value = comps / total_s
+
+    # ---- roofline of the local join (per rank: this rank's comparisons / its launch time)
+    peak, peak_src = peaks()
+    bytes_per_cmp = 4 * d
+    achieved = bytes_per_cmp * join_comps / (join_ms / 1e3) / 1e9 if join_ms > 0 else 0.0
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": ncu_traffic(args.config), "kernel": "knnd_local_join (classify + size-class join launches)",
+            "bytes_per_comparison": bytes_per_cmp, "peak_source": peak_src,
+            "comparisons_per_s": join_comps / (join_ms / 1e3) if join_ms > 0 else 0.0,
+            "share_of_step": join_ms / sum(step_ms) if step_ms else None}
+
+    # ---- end to end through the public API from host buffers
+    e2e_s, e2e_comps = 0.0, 0
+    h2d = d2h = 0
+    for i in range(args.e2e_steps + 1):
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rs_e = b2.KlRankingSystem(pts, validate=False)
+        friends, hist = b2.run(b2.Dataset(pts), rs_e, cfg)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        rs_e.release()
+        if i == 0:
+            continue  # first call warms the pinned-memory pool
+        e2e_s += dt
+        e2e_comps += sum(h.comparisons for h in hist)
+        s = eng.shard
+        h2d = n * d * 8 + (s.hi - s.lo) * k * 4 + max_rounds * 3 * cfg.fcc_sample_count * 4
+        d2h = n * k * 4 + 64 * len(hist)
+    tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    e2e_value = e2e_comps / tt.item() if tt.item() > 0 else 0.0
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        tab, init, csr, sample = cpu_sample_setup(n, d, k, seed)
+        c, s_ = cpu_sample_run(tab, init, csr, sample)
+        cores = cpu_threads()
+        cpu = {"value": c / s_, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"round-1 local join of {sample.size} sampled anchors of {args.config.upper()}, "
+                         f"C oracle (oracle/knnd_oracle.c), {cores} threads, {s_:.2f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": statistics.mean(step_ms), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32 screen + f64 exact rescoring",
+            "data": "synthetic (seeded flat-Dirichlet simplex points, reference generator stream)",
+            "config": {"workload": workload_desc(args.config, n, d, k), "n": n, "d": d, "k": k, "seed": seed,
+                       "rounds_per_step": rounds, "comparisons_per_step": comps // max(args.steps, 1),
+                       "time_to_termination_ms": statistics.mean(step_ms),
+                       "l2": "flushed (256 MiB write) before every step",
+                       "parallelism": f"row-shard x{world}" + (" + NCCL all-gather" if world > 1 else "")},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "time_to_termination_s": tt.item() / max(args.e2e_steps, 1)},
+            "gpu_launches": launches_total,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def ncu_traffic(config):
+    """dram bytes per local-join launch from the committed ncu summary, if any."""
+    path = os.path.join(ROOT, "profiles", f"ncu_join_{config}.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as fh:
+        return json.load(fh).get("dram_bytes_per_launch")
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        b200_arm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -153,3 +153,24 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 }
 
 }  // namespace knnd
+
+namespace knnd {
+
+// ---------------------------------------------------------------------------
+// cp.async (LDGSTS) gathers into shared memory.  Rows are copied in
+// row-contiguous 16 B (or 8 B) chunks so one warp instruction touches a few
+// 128 B lines instead of 32 scattered ones (L1TEX wavefronts, not DRAM, bound
+// a lane-per-row gather).
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+}  // namespace knnd

@@ -1,29 +1,35 @@
 // K2+K3+K4 — the fused local join (descent.py:230-242 driven by 262-314).
 //
-// Per anchor x (one thread group of G threads per anchor, persistent grid):
-//   phase 0  stage S = F(x) ++ C(x) and the anchor row (x64, x32) in smem
+// Per anchor x:
+//   phase 0  stage S = F(x) ++ C(x) and the anchor row (x32, x64) in smem
 //   phase 1  enumerate the (K+c)(K+1) pre-dedup ids  S ++ F(S)  and insert
-//            every id != x into an open-addressing hash table; first
-//            inserters append to the unique list U (warp-aggregated)
-//   phase 2  screen: for every y in U gather the fp32 log row (float4),
-//            ce = -sum x32*log32 and ab = sum |x32*log32| (FP32 FFMA);
-//            the fp64 cross entropy lies in [ce - c*ab, ce + c*ab],
-//            c = (ld+8)*2^-24 (rigorous: all-one-sign products, one rounding
-//            of x and of log per term plus the FMA chain).  Each warp keeps a
-//            running top-K of the upper bounds in registers (bitonic warp
-//            merge); the block merges them -> T = K-th smallest upper bound.
-//   phase 3  R = { y : lower(y) <= T }  (|R| >= K, typically K..K+2)
-//   phase 4  rescore R exactly in fp64 (fp64 log rows) and keep the K
-//            smallest (score, id) — the reference's stable argsort order —
-//            then write the row, |U| and the order-sensitive change flag.
+//            every id != x into an open-addressing hash table in shared
+//            memory; the first inserter of an id appends it to the unique
+//            list U.  |U| is the reference's `comparisons` (descent.py:275).
+//   phase 2  screen: gather the fp32 log row of every y in U into shared
+//            memory (cp.async, row-contiguous chunks) and compute
+//            ce = -sum x32*log32, ab = sum |x32*log32| (FP32 FFMA).  The fp64
+//            cross entropy CE lies within c*ab of ce, c = (ld+8)*2^-24
+//            (rigorous: all products of one sign, one rounding of x and of
+//            log per term plus the FMA chain).
+//   phase 2b T >= the K-th smallest ce.  Then K candidates have CE <= T + c*am
+//            (am = max ab), so every exact top-K member has ce <= T + 2*c*am.
+//   phase 3  R = { y : ce(y) <= T + 2*c*am }   (|R| >= K, typically K..K+2)
+//   phase 4  gather the fp64 log rows of R (cp.async), rescore exactly and
+//            keep the K smallest (score, id) — the reference's stable-argsort
+//            order — then write the row, |U| and the order-sensitive change flag.
 //
-// Result: identical to ranking all of U by exact fp64 scores, at the gather
+// So the output equals ranking all of U by exact fp64 scores, at the gather
 // cost of one fp32 row per comparison plus one fp64 row per member of R.
 //
+// Rows are gathered into shared memory in row-contiguous chunks: a warp
+// instruction then touches a few 128 B lines instead of 32 scattered ones —
+// with one lane per row the gather is bound by L1TEX wavefronts, not DRAM.
+//
 // Anchors are binned by their pre-dedup bound P = (K+c)(K+1):
-//   class A  G=128, table of H_A slots in shared memory
-//   class B  G=256, table of H_B slots in shared memory
-//   class L  G=512, table in a global-memory slab per block (hubs)
+//   W1, W2  one warp per anchor, private smem slab (table of H1 / 2*H1 slots)
+//   B       one 256-thread block per anchor, table of up to 2^15 slots in smem
+//   L       one 512-thread block per anchor, table in a global-memory slab
 #include "common.cuh"
 #include "score.cuh"
 
@@ -31,7 +37,6 @@ namespace knnd {
 
 constexpr int EMPTY = -1;
 constexpr int UNR1 = 4;  // pre-dedup ids loaded per thread before inserting
-constexpr int UNR2 = 2;  // candidate rows gathered per thread per step
 
 struct JoinParams {
   const double *__restrict__ points;
@@ -50,21 +55,21 @@ struct JoinParams {
   float band;
 };
 
-template <int G>
-__device__ __forceinline__ void group_sync() {
-  if (G == 32)
-    __syncwarp();
-  else
-    __syncthreads();
-}
+__host__ __device__ inline size_t al16(size_t v) { return (v + 15) & ~(size_t)15; }
 
-__device__ __forceinline__ bool hash_insert(int32_t *table, int y, unsigned shift, unsigned mask) {
-  unsigned h = ((unsigned)y * 0x9E3779B1u) >> shift;
+// ---------------------------------------------------------------------------
+// shared device pieces
+
+__device__ __forceinline__ unsigned hash_slot(int y, unsigned shift) { return ((unsigned)y * 0x9E3779B1u) >> shift; }
+
+// block-wide insert (several warps share the table): CAS
+__device__ __forceinline__ bool hash_insert_cas(int32_t *table, int y, unsigned shift, unsigned mask) {
+  unsigned h = hash_slot(y, shift);
   while (true) {
-    int cur = *reinterpret_cast<volatile int32_t *>(table + h);
+    const int cur = *reinterpret_cast<volatile int32_t *>(table + h);
     if (cur == y) return false;
     if (cur == EMPTY) {
-      int prev = atomicCAS(table + h, EMPTY, y);
+      const int prev = atomicCAS(table + h, EMPTY, y);
       if (prev == EMPTY) return true;
       if (prev == y) return false;
     }
@@ -74,9 +79,9 @@ __device__ __forceinline__ bool hash_insert(int32_t *table, int y, unsigned shif
 
 // warp-aggregated append of `val` (where `take`) to list[*counter ...]
 __device__ __forceinline__ void warp_append(bool take, int val, int *counter, int32_t *list, int lane) {
-  unsigned m = __ballot_sync(FULL, take);
+  const unsigned m = __ballot_sync(FULL, take);
   if (m) {
-    int leader = __ffs(m) - 1;
+    const int leader = __ffs(m) - 1;
     int base = 0;
     if (lane == leader) base = atomicAdd(counter, __popc(m));
     base = __shfl_sync(FULL, base, leader);
@@ -84,23 +89,133 @@ __device__ __forceinline__ void warp_append(bool take, int val, int *counter, in
   }
 }
 
-// shared-memory layout (bytes); identical on host and device
+// issue cp.async copies of the fp32 log rows of ids[0..nrow) into stage
+// (row stride ld floats), 16 B chunks, consecutive lanes on consecutive chunks
+template <int NV4>
+__device__ __forceinline__ void stage_rows_f32(float *stage, const float *__restrict__ log32, const int32_t *ids,
+                                               int nrow, int ld, int lane) {
+  const int nv4 = NV4 > 0 ? NV4 : (ld >> 2);
+  const int nchunk = nrow * nv4;
+  for (int c = lane; c < nchunk; c += 32) {
+    const int r = c / nv4, part = c - r * nv4;
+    const int y = ids[r];
+    cp_async16(stage + r * ld + part * 4, log32 + (int64_t)y * ld + part * 4);
+  }
+}
+
+// ce = -sum x*l and ab = sum |x*l| of one staged row (left to right)
+template <int NV4>
+__device__ __forceinline__ void screen_row(const float *row, const float *x32, int ld, float &ce, float &ab) {
+  const float4 *r4 = reinterpret_cast<const float4 *>(row);
+  const float4 *x4 = reinterpret_cast<const float4 *>(x32);
+  const int nv4 = NV4 > 0 ? NV4 : (ld >> 2);
+  float a = 0.f, b = 0.f;
+#pragma unroll
+  for (int q = 0; q < (NV4 > 0 ? NV4 : 64); ++q) {
+    if (NV4 == 0 && q >= nv4) break;
+    const float4 xv = x4[q];
+    const float4 l = r4[q];
+    a = fmaf(-xv.x, l.x, a);
+    a = fmaf(-xv.y, l.y, a);
+    a = fmaf(-xv.z, l.z, a);
+    a = fmaf(-xv.w, l.w, a);
+    b = fmaf(xv.x, fabsf(l.x), b);
+    b = fmaf(xv.y, fabsf(l.y), b);
+    b = fmaf(xv.z, fabsf(l.z), b);
+    b = fmaf(xv.w, fabsf(l.w), b);
+  }
+  ce = a;
+  ab = b;
+}
+
+// issue cp.async copies of the fp64 log rows of ids[0..nrow) into stage
+// (row stride sd doubles, sd odd to spread banks), 8 B chunks
+__device__ __forceinline__ void stage_rows_f64(double *stage, int sd, const double *__restrict__ log64,
+                                               const int32_t *ids, int nrow, int d, int lane) {
+  const int nchunk = nrow * d;
+  const int rq = 32 / d, rr = 32 - rq * d;
+  int r = lane / d, j = lane - r * d;
+  for (int c = lane; c < nchunk; c += 32) {
+    cp_async8(stage + r * sd + j, log64 + (int64_t)ids[r] * d + j);
+    r += rq;
+    j += rr;
+    if (j >= d) {
+      j -= d;
+      ++r;
+    }
+  }
+}
+
+// exact fp64 score from a staged row: same left-to-right FMA order as exact_score
+__device__ __forceinline__ double exact_from_row(const double *row, const double *x64, int d, double xl) {
+  double acc = 0.0;
+  for (int j = 0; j < d; ++j) acc = fma(x64[j], row[j], acc);
+  return xl - acc;
+}
+
+// emit the sorted row (lanes hold the exact top-K), return the change flag
+template <int KPL>
+__device__ __forceinline__ bool emit_row(const JoinParams &p, const WarpTopK<KeyD, KPL> &ex, int x, int64_t xr,
+                                         int lane) {
+  const int K = p.K;
+  bool diff = false;
+#pragma unroll
+  for (int q = 0; q < KPL; ++q) {
+    const int i = q * 32 + lane;
+    if (i < K) {
+      const KeyD kq = ex.b[q];
+      p.out_ids[xr * K + i] = kq.id;
+      if (p.out_kl) p.out_kl[xr * K + i] = kq.s;
+      diff |= kq.id != __ldg(p.F + (int64_t)x * K + i);
+    }
+  }
+  return __any_sync(FULL, diff);
+}
+
+// phase 4 for one warp: exact rescoring of R = ids[0..nR) through stage64
+template <int KPL>
+__device__ __forceinline__ void exact_rank(const JoinParams &p, WarpTopK<KeyD, KPL> &ex, const int32_t *ids, int nR,
+                                           double *stage64, int rcap, const double *x64, double xl, int lane) {
+  const int d = p.d, sd = d | 1;
+  ex.init();
+  for (int b = 0; b < nR; b += rcap) {
+    const int nrow = min(rcap, nR - b);
+    stage_rows_f64(stage64, sd, p.log64, ids + b, nrow, d, lane);
+    cp_async_wait_all();
+    __syncwarp();
+    KeyD key = KeyD::inf();
+    if (lane < nrow) {
+      key.s = exact_from_row(stage64 + lane * sd, x64, d, xl);
+      key.id = ids[b + lane];
+    }
+    __syncwarp();
+    ex.insert(key, p.K, lane);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// block-per-anchor kernel (classes B and L)
+
 struct SmemLayout {
-  size_t x32, x64, mbuf, S, table, list, total;
+  size_t x32, x64, red, hist, stage, S, table, list, total;
 };
 
-__host__ __device__ inline size_t al16(size_t v) { return (v + 15) & ~(size_t)15; }
+constexpr int NBIN = 256;        // histogram-select buckets per pass
+constexpr int LSTAGE_ROWS = 16;  // per-warp staged rows in the global-table class
 
-__host__ __device__ inline SmemLayout smem_layout(int G, int KPL, bool gtab, int d, int ld, int H, int SW) {
+__host__ __device__ inline SmemLayout smem_layout(int G, bool gtab, int d, int ld, int H, int SW) {
   SmemLayout L;
-  size_t o = 16;  // header: cnt, rcnt, theta
+  size_t o = 64;  // header ints: [0] |U| [1] |R| [2] b1 [3] before1 [4] b2
   L.x32 = o;
   o = al16(o + (size_t)ld * 4);
   L.x64 = o;
   o = al16(o + (size_t)d * 8);
-  L.mbuf = o;
-  o = al16(o + (G > 32 ? (size_t)(G / 32) * 32 * KPL * 4 : 0));
+  L.red = o;
+  o = al16(o + (size_t)(G / 32) * 4 * 4);
+  L.hist = o;
+  o = al16(o + (size_t)2 * NBIN * 4);
   if (!gtab) {
+    L.stage = 0;  // staging uses the (dead) table
     L.S = o;
     o = al16(o + (size_t)SW * 4);
     L.table = o;
@@ -108,94 +223,47 @@ __host__ __device__ inline SmemLayout smem_layout(int G, int KPL, bool gtab, int
     L.list = o;
     o = al16(o + (size_t)(H / 2) * 4);
   } else {
+    size_t st = (size_t)(G / 32) * LSTAGE_ROWS * ld * 4;
+    const size_t st64 = (size_t)32 * (d | 1) * 8;
+    if (st < st64) st = st64;
+    L.stage = o;
+    o = al16(o + st);
     L.S = L.table = L.list = 0;
   }
   L.total = o;
   return L;
 }
 
-// screening pass over U for one anchor; returns this warp's top-K of upper bounds
-template <int G, int NV4, int KPL>
-__device__ __forceinline__ void screen(const JoinParams &p, const int32_t *list, float *scores, int U,
-                                       const float *x32, WarpTopK<KeyF, KPL> &top, int tid, int lane) {
-  const float c = p.band;
-  const int K = p.K;
-  const float4 *x4 = reinterpret_cast<const float4 *>(x32);
-  const int step = G * UNR2;
-  const int iters = (U + step - 1) / step;
-  for (int it = 0; it < iters; ++it) {
-    int kk[UNR2];
-    float ce[UNR2], ab[UNR2];
-    if constexpr (NV4 > 0) {
-      float4 row[UNR2][NV4];
+// warp 0: the bucket holding the target-th smallest (1-based) of hist[0..NBIN)
+// -> hdr[slot] = bucket, hdr[slot+1] = count strictly below it
+__device__ __forceinline__ void hist_find(const int *hist, int target, int *hdr, int slot, int lane) {
+  constexpr int PER = NBIN / 32;
+  int c[PER], tot = 0;
 #pragma unroll
-      for (int u = 0; u < UNR2; ++u) {
-        kk[u] = it * step + u * G + tid;
-        if (kk[u] < U) {
-          const int y = list[kk[u]];
-          const float4 *r4 = reinterpret_cast<const float4 *>(p.log32 + (int64_t)y * NV4 * 4);
+  for (int i = 0; i < PER; ++i) {
+    c[i] = hist[lane * PER + i];
+    tot += c[i];
+  }
+  int inc = tot;
 #pragma unroll
-          for (int q = 0; q < NV4; ++q) row[u][q] = __ldg(r4 + q);
-        } else {
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(FULL, inc, o);
+    if (lane >= o) inc += u;
+  }
+  const unsigned m = __ballot_sync(FULL, inc >= target);
+  const int first = m ? __ffs(m) - 1 : 31;
+  if (lane == first) {
+    int run = inc - tot, b = PER - 1;
 #pragma unroll
-          for (int q = 0; q < NV4; ++q) row[u][q] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+    for (int i = 0; i < PER; ++i) {
+      if (run + c[i] >= target) {
+        b = i;
+        break;
       }
-#pragma unroll
-      for (int u = 0; u < UNR2; ++u) {
-        float a = 0.f, b = 0.f;
-#pragma unroll
-        for (int q = 0; q < NV4; ++q) {
-          const float4 xv = x4[q];
-          const float4 l = row[u][q];
-          a = fmaf(-xv.x, l.x, a);
-          a = fmaf(-xv.y, l.y, a);
-          a = fmaf(-xv.z, l.z, a);
-          a = fmaf(-xv.w, l.w, a);
-          b = fmaf(xv.x, fabsf(l.x), b);
-          b = fmaf(xv.y, fabsf(l.y), b);
-          b = fmaf(xv.z, fabsf(l.z), b);
-          b = fmaf(xv.w, fabsf(l.w), b);
-        }
-        ce[u] = a;
-        ab[u] = b;
-      }
-    } else {
-      const int nv4 = p.ld >> 2;
-#pragma unroll
-      for (int u = 0; u < UNR2; ++u) {
-        kk[u] = it * step + u * G + tid;
-        float a = 0.f, b = 0.f;
-        if (kk[u] < U) {
-          const int y = list[kk[u]];
-          const float4 *r4 = reinterpret_cast<const float4 *>(p.log32 + (int64_t)y * p.ld);
-          for (int q = 0; q < nv4; ++q) {
-            const float4 xv = x4[q];
-            const float4 l = __ldg(r4 + q);
-            a = fmaf(-xv.x, l.x, a);
-            a = fmaf(-xv.y, l.y, a);
-            a = fmaf(-xv.z, l.z, a);
-            a = fmaf(-xv.w, l.w, a);
-            b = fmaf(xv.x, fabsf(l.x), b);
-            b = fmaf(xv.y, fabsf(l.y), b);
-            b = fmaf(xv.z, fabsf(l.z), b);
-            b = fmaf(xv.w, fabsf(l.w), b);
-          }
-        }
-        ce[u] = a;
-        ab[u] = b;
-      }
+      run += c[i];
     }
-#pragma unroll
-    for (int u = 0; u < UNR2; ++u) {
-      KeyF up = KeyF::inf();
-      if (kk[u] < U) {
-        const float delta = c * ab[u];
-        scores[kk[u]] = ce[u] - delta;
-        up.v = ce[u] + delta;
-      }
-      top.insert(up, K, lane);
-    }
+    hdr[slot] = lane * PER + b;
+    hdr[slot + 1] = run;
   }
 }
 
@@ -208,21 +276,35 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int H = 1 << logH;
   const unsigned shift = 32u - (unsigned)logH;
-  const SmemLayout L = smem_layout(G, KPL, GTAB, p.d, p.ld, H, SW);
+  const SmemLayout L = smem_layout(G, GTAB, p.d, p.ld, H, SW);
   int *hdr = reinterpret_cast<int *>(sm);
   float *x32 = reinterpret_cast<float *>(sm + L.x32);
   double *x64 = reinterpret_cast<double *>(sm + L.x64);
-  float *mbuf = reinterpret_cast<float *>(sm + L.mbuf);
+  float *red = reinterpret_cast<float *>(sm + L.red);
+  int *hist = reinterpret_cast<int *>(sm + L.hist);
+  int *hist2 = hist + NBIN;
   int32_t *S, *table, *list;
+  float *wstage;  // this warp's fp32 staging rows
+  double *stage64;
+  int wrows, rcap64;
   if constexpr (GTAB) {
     int32_t *slab = gslab + (int64_t)blockIdx.x * slab_ints;
     S = slab;
     table = slab + SW;
     list = table + H;
+    wrows = LSTAGE_ROWS;
+    wstage = reinterpret_cast<float *>(sm + L.stage) + (size_t)warp * LSTAGE_ROWS * p.ld;
+    stage64 = reinterpret_cast<double *>(sm + L.stage);
+    rcap64 = 32;
   } else {
     S = reinterpret_cast<int32_t *>(sm + L.S);
     table = reinterpret_cast<int32_t *>(sm + L.table);
     list = reinterpret_cast<int32_t *>(sm + L.list);
+    const int per_warp_floats = (H / 2) / W;  // upper half of the table, split over warps
+    wrows = min(32, per_warp_floats / p.ld);
+    wstage = reinterpret_cast<float *>(table + H / 2) + (size_t)warp * per_warp_floats;
+    stage64 = reinterpret_cast<double *>(table);  // lower half, free in phase 4
+    rcap64 = min(32, (2 * H) / ((p.d | 1) * 8));
   }
   const int K = p.K, K1 = K + 1;
   const int d = p.d, ld = p.ld;
@@ -239,13 +321,12 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     const int nS = K + c;
     const int total = nS * K1;
 
-    // ---- phase 0: clear table, stage S and the anchor row
-    if constexpr (GTAB) {
+    // ---- phase 0: clear table + histograms, stage S and the anchor row
+    {
       int4 *t4 = reinterpret_cast<int4 *>(table);
       for (int i = tid; i < (H >> 2); i += G) t4[i] = make_int4(EMPTY, EMPTY, EMPTY, EMPTY);
-    } else {
-      for (int i = tid; i < H; i += G) table[i] = EMPTY;
     }
+    for (int i = tid; i < 2 * NBIN; i += G) hist[i] = 0;
     for (int i = tid; i < nS; i += G) S[i] = i < K ? __ldg(p.F + (int64_t)x * K + i) : __ldg(p.indices + c0 + (i - K));
     for (int i = tid; i < ld; i += G) x32[i] = i < d ? (float)__ldg(p.points + (int64_t)x * d + i) : 0.f;
     for (int i = tid; i < d; i += G) x64[i] = __ldg(p.points + (int64_t)x * d + i);
@@ -253,8 +334,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
       hdr[0] = 0;
       hdr[1] = 0;
     }
-    if constexpr (GTAB) __threadfence_block();
-    group_sync<G>();
+    __syncthreads();
 
     // ---- phase 1: pre-dedup enumeration + hash dedup
     {
@@ -281,44 +361,78 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
         for (int u = 0; u < UNR1; ++u) {
           const int y = id[u];
           bool isnew = false;
-          if (y >= 0 && y != x) isnew = hash_insert(table, y, shift, (unsigned)H - 1u);
+          if (y >= 0 && y != x) isnew = hash_insert_cas(table, y, shift, (unsigned)H - 1u);
           warp_append(isnew, y, &hdr[0], list, lane);
         }
       }
     }
-    if constexpr (GTAB) __threadfence_block();
-    group_sync<G>();
+    __syncthreads();
     const int U = hdr[0];
 
-    // ---- phase 2: fp32 screening, per-warp top-K of upper bounds
-    float *scores = reinterpret_cast<float *>(table);  // table is dead now
-    WarpTopK<KeyF, KPL> top;
-    top.init();
-    screen<G, NV4, KPL>(p, list, scores, U, x32, top, tid, lane);
-    if constexpr (W > 1) {
+    // ---- phase 2: fp32 screen, one staged batch of rows per warp at a time
+    float *scores = reinterpret_cast<float *>(table);  // the hash table is dead now
+    float mn = __int_as_float(0x7f800000), mx = -mn, am = 0.f;
+    for (int k0 = warp * wrows; k0 < U; k0 += W * wrows) {
+      const int nrow = min(wrows, U - k0);
+      stage_rows_f32<NV4>(wstage, p.log32, list + k0, nrow, ld, lane);
+      cp_async_wait_all();
+      __syncwarp();
+      if (lane < nrow) {
+        float ce, ab;
+        screen_row<NV4>(wstage + lane * ld, x32, ld, ce, ab);
+        scores[k0 + lane] = ce;
+        mn = fminf(mn, ce);
+        mx = fmaxf(mx, ce);
+        am = fmaxf(am, ab);
+      }
+      __syncwarp();
+    }
 #pragma unroll
-      for (int q = 0; q < KPL; ++q) {
-        const int i = q * 32 + lane;
-        mbuf[warp * 32 * KPL + i] = (i < K) ? top.b[q].v : KeyF::inf().v;
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = fminf(mn, __shfl_xor_sync(FULL, mn, o));
+      mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
+      am = fmaxf(am, __shfl_xor_sync(FULL, am, o));
+    }
+    if (lane == 0) {
+      red[warp * 4 + 0] = mn;
+      red[warp * 4 + 1] = mx;
+      red[warp * 4 + 2] = am;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      mn = fminf(mn, red[w * 4 + 0]);
+      mx = fmaxf(mx, red[w * 4 + 1]);
+      am = fmaxf(am, red[w * 4 + 2]);
+    }
+
+    // ---- phase 2b: T >= the K-th smallest ce (two histogram passes)
+    float T = mx;
+    const float range = mx - mn;
+    if (U > 2 * K && range > 0.f) {
+      const float inv = (float)NBIN / range;
+      for (int k = tid; k < U; k += G) {
+        const float t = (scores[k] - mn) * inv;
+        atomicAdd(&hist[min(NBIN - 1, (int)t)], 1);
       }
       __syncthreads();
-      if (warp == 0) {
-        for (int w2 = 1; w2 < W; ++w2) {
-#pragma unroll
-          for (int q = 0; q < KPL; ++q) top.insert(KeyF{mbuf[w2 * 32 * KPL + q * 32 + lane]}, K, lane);
-        }
+      if (warp == 0) hist_find(hist, K, hdr, 2, lane);
+      __syncthreads();
+      const int b1 = hdr[2], before = hdr[3];
+      for (int k = tid; k < U; k += G) {
+        const float t = (scores[k] - mn) * inv;
+        if (min(NBIN - 1, (int)t) == b1) atomicAdd(&hist2[min(NBIN - 1, (int)((t - (float)b1) * (float)NBIN))], 1);
       }
+      __syncthreads();
+      if (warp == 0) hist_find(hist2, K - before, hdr, 4, lane);
+      __syncthreads();
+      const int b2 = hdr[4];
+      T = mn + ((float)b1 + (float)(b2 + 1) * (1.0f / NBIN)) / inv;
+      T += (fabsf(T) + range) * 1e-6f;  // covers the rounding of t and of this line
     }
-    if (warp == 0) {
-      const float kth = top.get(K - 1).v;
-      const float theta = __fadd_ru(kth, __fmul_ru(fabsf(kth), 1e-6f));
-      if (lane == 0) hdr[2] = __float_as_int(theta);
-    }
-    if constexpr (GTAB) __threadfence_block();
-    group_sync<G>();
+    const float theta = T + 2.f * p.band * am + fabsf(T) * 1e-6f;
 
     // ---- phase 3: collect every candidate the screen cannot exclude
-    const float theta = __int_as_float(hdr[2]);
     int32_t *R = table + (H >> 1);
     {
       const int iters = (U + G - 1) / G;
@@ -328,37 +442,14 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
         warp_append(take, take ? list[k] : 0, &hdr[1], R, lane);
       }
     }
-    if constexpr (GTAB) __threadfence_block();
-    group_sync<G>();
+    __syncthreads();
     const int nR = hdr[1];
 
-    // ---- phase 4: exact fp64 ranking of R, output
+    // ---- phase 4: exact fp64 ranking of R, output (warp 0)
     if (warp == 0) {
       WarpTopK<KeyD, KPL> ex;
-      ex.init();
-      const double xl = __ldg(p.xlogx + x);
-      for (int b = 0; b < nR; b += 32) {
-        const int r = b + lane;
-        KeyD key = KeyD::inf();
-        if (r < nR) {
-          const int y = R[r];
-          key.s = exact_score(x64, p.log64 + (int64_t)y * d, d, xl);
-          key.id = y;
-        }
-        ex.insert(key, K, lane);
-      }
-      bool diff = false;
-#pragma unroll
-      for (int q = 0; q < KPL; ++q) {
-        const int i = q * 32 + lane;
-        if (i < K) {
-          const KeyD kq = ex.b[q];
-          p.out_ids[xr * K + i] = kq.id;
-          if (p.out_kl) p.out_kl[xr * K + i] = kq.s;
-          diff |= kq.id != __ldg(p.F + (int64_t)x * K + i);
-        }
-      }
-      diff = __any_sync(FULL, diff);
+      exact_rank<KPL>(p, ex, R, nR, stage64, rcap64, x64, __ldg(p.xlogx + x), lane);
+      const bool diff = emit_row<KPL>(p, ex, x, xr, lane);
       if (lane == 0) {
         acc_comp += (unsigned long long)U;
         acc_changed += diff ? 1ull : 0ull;
@@ -366,7 +457,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
         if (p.out_ucount) p.out_ucount[xr] = U;
       }
     }
-    group_sync<G>();
+    __syncthreads();
   }
   if (tid == 0) {
     if (acc_comp) atomicAdd(&p.tally[0], acc_comp);
@@ -375,9 +466,218 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
   }
 }
 
-// bin the anchors of [lo, hi) by pre-dedup bound P = (K+c)(K+1)
-__global__ void classify_kernel(const int64_t *__restrict__ indptr, int64_t m, int64_t lo, int K, int64_t PA,
-                                int64_t PB, int32_t *__restrict__ lists, int32_t *__restrict__ counts) {
+// ---------------------------------------------------------------------------
+// warp-per-anchor kernel (classes W1, W2).  One warp owns one anchor and a
+// private smem slab, so nothing waits on a block barrier and the unique list
+// needs no atomics:
+//   * dedup: __match_any_sync elects one lane per distinct id in a batch;
+//     leaders claim slots by store-then-verify (a slot keeps the last id
+//     written; losers probe on) — no shared-memory atomics
+//   * threshold: every lane keeps its 2*KPL smallest screened values; the
+//     K-th smallest of that subset is >= the K-th smallest overall, so it is
+//     a valid T (tight unless one lane holds > 2*KPL of the best K)
+
+struct WarpSlab {
+  size_t x32, x64, S, table, list, total;
+};
+
+__host__ __device__ inline WarpSlab warp_slab(int d, int ld, int H, int SW) {
+  WarpSlab L;
+  size_t o = 0;
+  L.x32 = o;
+  o = al16(o + (size_t)ld * 4);
+  L.x64 = o;
+  o = al16(o + (size_t)d * 8);
+  L.S = o;
+  o = al16(o + (size_t)SW * 4);
+  L.table = o;
+  o = al16(o + (size_t)H * 4);
+  L.list = o;
+  o = al16(o + (size_t)(H / 2) * 4);
+  L.total = o;
+  return L;
+}
+
+template <int NV4, int KPL>
+__global__ void __launch_bounds__(128) join_warp_kernel(JoinParams p, const int32_t *__restrict__ alist,
+                                                        const int32_t *__restrict__ acount, int logH, int SW) {
+  constexpr int Q = 2 * KPL;  // per-lane kept screened values
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int H = 1 << logH;
+  const unsigned shift = 32u - (unsigned)logH, hmask = (unsigned)H - 1u;
+  const WarpSlab L = warp_slab(p.d, p.ld, H, SW);
+  unsigned char *base = sm + (size_t)warp * L.total;
+  float *x32 = reinterpret_cast<float *>(base + L.x32);
+  double *x64 = reinterpret_cast<double *>(base + L.x64);
+  int32_t *S = reinterpret_cast<int32_t *>(base + L.S);
+  int32_t *table = reinterpret_cast<int32_t *>(base + L.table);
+  int32_t *list = reinterpret_cast<int32_t *>(base + L.list);
+  float *scores = reinterpret_cast<float *>(table);            // phase 2-3: [0, U)
+  float *stage = reinterpret_cast<float *>(table + (H >> 1));  // phase 2: upper half
+  double *stage64 = reinterpret_cast<double *>(table);         // phase 4: whole table
+  const int K = p.K, K1 = K + 1;
+  const int d = p.d, ld = p.ld, sd = d | 1;
+  const int rows = min(32, (2 * H) / (ld * 4));
+  const int rcap64 = min(32, (4 * H) / (sd * 8));
+  const int Gq = 32 / K1, Gr = 32 % K1;
+  const int s_init = lane / K1, j_init = lane % K1;
+  unsigned long long acc_comp = 0, acc_changed = 0, acc_bad = 0;
+  const int count = *acount;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+
+  for (int a = blockIdx.x * (blockDim.x >> 5) + warp; a < count; a += nwarps) {
+    const int x = alist[a];
+    const int64_t xr = (int64_t)x - p.lo;
+    const int64_t c0 = p.indptr[xr];
+    const int c = (int)(p.indptr[xr + 1] - c0);
+    const int nS = K + c;
+    const int total = nS * K1;
+
+    // ---- phase 0
+    {
+      int4 *t4 = reinterpret_cast<int4 *>(table);
+      for (int i = lane; i < (H >> 2); i += 32) t4[i] = make_int4(EMPTY, EMPTY, EMPTY, EMPTY);
+    }
+    for (int i = lane; i < nS; i += 32) S[i] = i < K ? __ldg(p.F + (int64_t)x * K + i) : __ldg(p.indices + c0 + (i - K));
+    for (int i = lane; i < ld; i += 32) x32[i] = i < d ? (float)__ldg(p.points + (int64_t)x * d + i) : 0.f;
+    for (int i = lane; i < d; i += 32) x64[i] = __ldg(p.points + (int64_t)x * d + i);
+    __syncwarp();
+
+    // ---- phase 1: dedup (no atomics)
+    int U = 0;
+    {
+      int s = s_init, j = j_init;
+      for (int e0 = 0; e0 < total; e0 += 32 * UNR1) {
+        int id[UNR1];
+#pragma unroll
+        for (int u = 0; u < UNR1; ++u) {
+          const int e = e0 + u * 32 + lane;
+          id[u] = -1;
+          if (e < total) {
+            const int v = S[s];
+            id[u] = (j == 0) ? v : __ldg(p.F + (int64_t)v * K + (j - 1));
+          }
+          s += Gq;
+          j += Gr;
+          if (j >= K1) {
+            j -= K1;
+            ++s;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < UNR1; ++u) {
+          const int y = id[u];
+          const bool valid = y >= 0 && y != x;
+          const unsigned grp = __match_any_sync(FULL, valid ? y : -1 - lane);
+          bool pending = valid && (__ffs(grp) - 1 == lane);
+          bool isnew = false;
+          unsigned h = hash_slot(y, shift);
+          while (__any_sync(FULL, pending)) {
+            bool claim = false;
+            if (pending) {
+              const int cur = table[h];
+              if (cur == y) {
+                pending = false;
+              } else if (cur == EMPTY) {
+                claim = true;
+                table[h] = y;
+              } else {
+                h = (h + 1) & hmask;
+              }
+            }
+            __syncwarp();
+            if (claim) {
+              if (table[h] == y) {
+                pending = false;
+                isnew = true;
+              } else {
+                h = (h + 1) & hmask;
+              }
+            }
+            __syncwarp();
+          }
+          const unsigned m = __ballot_sync(FULL, isnew);
+          if (isnew) list[U + __popc(m & lanemask_lt())] = y;
+          U += __popc(m);
+        }
+      }
+    }
+    __syncwarp();
+
+    // ---- phase 2: screen; per-lane Q smallest, max |x log y| sum
+    float best[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) best[q] = __int_as_float(0x7f800000);
+    float am = 0.f;
+    for (int k0 = 0; k0 < U; k0 += rows) {
+      const int nrow = min(rows, U - k0);
+      stage_rows_f32<NV4>(stage, p.log32, list + k0, nrow, ld, lane);
+      cp_async_wait_all();
+      __syncwarp();
+      if (lane < nrow) {
+        float ce, ab;
+        screen_row<NV4>(stage + lane * ld, x32, ld, ce, ab);
+        scores[k0 + lane] = ce;
+        am = fmaxf(am, ab);
+        float v = ce;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {  // insertion into the sorted per-lane list
+          const float lo_ = fminf(best[q], v);
+          v = fmaxf(best[q], v);
+          best[q] = lo_;
+        }
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) am = fmaxf(am, __shfl_xor_sync(FULL, am, o));
+    float T = __int_as_float(0x7f800000);
+    if (rows * Q >= K) {  // otherwise the kept subset may hold fewer than K values
+      WarpTopK<KeyF, KPL> top;
+      top.init();
+#pragma unroll
+      for (int q = 0; q < Q; ++q) top.insert(KeyF{best[q]}, K, lane);
+      T = top.get(K - 1).v;  // >= the K-th smallest screened value (U >= K)
+    }
+    const float theta = T + 2.f * p.band * am + fabsf(T) * 1e-6f;
+
+    // ---- phase 3: R in place at the front of the list
+    int nR = 0;
+    for (int k0 = 0; k0 < U; k0 += 32) {
+      const int k = k0 + lane;
+      const bool take = k < U && scores[k] <= theta;
+      const int y = take ? list[k] : 0;
+      const unsigned m = __ballot_sync(FULL, take);
+      if (take) list[nR + __popc(m & lanemask_lt())] = y;
+      nR += __popc(m);
+    }
+    __syncwarp();
+
+    // ---- phase 4: exact fp64 ranking of R, output
+    WarpTopK<KeyD, KPL> ex;
+    exact_rank<KPL>(p, ex, list, nR, stage64, rcap64, x64, __ldg(p.xlogx + x), lane);
+    const bool diff = emit_row<KPL>(p, ex, x, xr, lane);
+    if (lane == 0) {
+      acc_comp += (unsigned long long)U;
+      acc_changed += diff ? 1ull : 0ull;
+      acc_bad += (U < K) ? 1ull : 0ull;
+      if (p.out_ucount) p.out_ucount[xr] = U;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    if (acc_comp) atomicAdd(&p.tally[0], acc_comp);
+    if (acc_changed) atomicAdd(&p.tally[1], acc_changed);
+    if (acc_bad) atomicAdd(&p.tally[2], acc_bad);
+  }
+}
+
+// bin the anchors of [lo, hi) by pre-dedup bound P = (K+c)(K+1):
+// class 0: P <= lim[0], class 1: P <= lim[1], class 2: P <= lim[2], class 3: rest
+__global__ void classify_kernel(const int64_t *__restrict__ indptr, int64_t m, int64_t lo, int K, int64_t lim0,
+                                int64_t lim1, int64_t lim2, int32_t *__restrict__ lists,
+                                int32_t *__restrict__ counts) {
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < m; base += stride) {
@@ -386,28 +686,29 @@ __global__ void classify_kernel(const int64_t *__restrict__ indptr, int64_t m, i
     if (xr < m) {
       const int64_t c = indptr[xr + 1] - indptr[xr];
       const int64_t P = ((int64_t)K + c) * (K + 1);
-      cls = P <= PA ? 0 : (P <= PB ? 1 : 2);
+      cls = P <= lim0 ? 0 : (P <= lim1 ? 1 : (P <= lim2 ? 2 : 3));
     }
 #pragma unroll
-    for (int k = 0; k < 3; ++k) warp_append(cls == k, (int)(lo + xr), counts + k, lists + (int64_t)k * m, lane);
+    for (int k = 0; k < 4; ++k) warp_append(cls == k, (int)(lo + xr), counts + k, lists + (int64_t)k * m, lane);
   }
 }
 
 // ---------------------------------------------------------------------------
 // host side
 
+// size classes: W1, W2 warp-per-anchor; B block (shared table); L block (global table)
 struct Plan {
   int kpl, nv4;
-  int logHA, logHB, logHL;
-  int swA, swB, swL;
-  int64_t PA, PB;
-  bool needB, needL;
+  int logH[4];
+  int sw[4];
+  int64_t lim[3];
+  bool need[4];
   int nslab;
   int64_t slab_ints;
   size_t lists_off, counts_off, slab_off, total;
 };
 
-constexpr int GA = 128, GB = 256, GL = 512;
+constexpr int WARP_BLOCK = 128, GB = 256, GL = 512;
 
 static int ilog2_ceil(int64_t v) {
   int l = 0;
@@ -419,27 +720,33 @@ static Plan make_plan(int64_t m, int d, int K, int max_indeg) {
   Plan P{};
   P.kpl = K <= 32 ? 1 : 2;
   P.nv4 = (d + 3) / 4;
-  // class A covers in-degrees up to ~1.5K, class B up to ~4x that
   const int64_t K1 = K + 1;
-  // (shared-memory caps: A <= 2^13 slots = 48 KB, B <= 2^15 slots = 192 KB)
-  P.logHA = ilog2_ceil(2 * K1 * (K + (3 * K) / 2));
-  if (P.logHA < 10) P.logHA = 10;
-  if (P.logHA > 13) P.logHA = 13;
-  P.logHB = P.logHA + 2 < 15 ? P.logHA + 2 : 15;
-  P.PA = ((int64_t)1 << P.logHA) / 2;
-  P.PB = ((int64_t)1 << P.logHB) / 2;
-  P.swA = (int)(P.PA / K1 + 1);
-  P.swB = (int)(P.PB / K1 + 1);
+  // W1 holds in-degrees up to ~1.4K (the bulk of a random K-out graph), W2 twice
+  // that; B (one block, shared table <= 2^15 slots) the tail; L the hubs.
+  int l1 = ilog2_ceil(2 * K1 * (K + (2 * K) / 5));
+  const int lstage = ilog2_ceil(64 * (int64_t)((d + 3) / 4 * 4));  // 32 staged fp32 rows fit in H/2 slots
+  if (l1 < lstage) l1 = lstage;
+  if (l1 < 9) l1 = 9;
+  if (l1 > 12) l1 = 12;
+  P.logH[0] = l1;
+  P.logH[1] = l1 + 1;
+  P.logH[2] = l1 + 3 < 15 ? l1 + 3 : 15;
+  for (int i = 0; i < 3; ++i) {
+    P.lim[i] = ((int64_t)1 << P.logH[i]) / 2;
+    P.sw[i] = (int)(P.lim[i] / K1 + 1);
+  }
   const int64_t Pmax = ((int64_t)K + max_indeg) * K1;
-  P.needB = Pmax > P.PA;
-  P.needL = Pmax > P.PB;
-  P.logHL = P.needL ? ilog2_ceil(2 * Pmax) : 0;
-  P.swL = (K + max_indeg + 31) & ~31;  // keeps the table int4-aligned in the slab
-  P.nslab = P.needL ? 2 * num_sms() : 0;
-  P.slab_ints = P.needL ? (int64_t)align_up((size_t)P.swL + ((size_t)3 << P.logHL) / 2, 64) : 0;
+  P.need[0] = true;
+  P.need[1] = Pmax > P.lim[0];
+  P.need[2] = Pmax > P.lim[1];
+  P.need[3] = Pmax > P.lim[2];
+  P.logH[3] = P.need[3] ? ilog2_ceil(2 * Pmax) : 0;
+  P.sw[3] = (K + max_indeg + 31) & ~31;  // keeps the table int4-aligned in the slab
+  P.nslab = P.need[3] ? 2 * num_sms() : 0;
+  P.slab_ints = P.need[3] ? (int64_t)align_up((size_t)P.sw[3] + ((size_t)3 << P.logH[3]) / 2, 64) : 0;
   size_t o = 0;
   P.lists_off = o;
-  o = align_up(o + (size_t)3 * m * 4, 256);
+  o = align_up(o + (size_t)4 * m * 4, 256);
   P.counts_off = o;
   o = align_up(o + 64, 256);
   P.slab_off = o;
@@ -452,7 +759,7 @@ template <int G, int NV4, int KPL, bool GTAB>
 static int launch_join(const JoinParams &p, const int32_t *alist, const int32_t *acount, int logH, int SW,
                        int32_t *gslab, int64_t slab_ints, int grid_cap, cudaStream_t st) {
   auto kern = join_kernel<G, NV4, KPL, GTAB>;
-  const SmemLayout L = smem_layout(G, KPL, GTAB, p.d, p.ld, 1 << logH, SW);
+  const SmemLayout L = smem_layout(G, GTAB, p.d, p.ld, 1 << logH, SW);
   const size_t smem = L.total;
   if (smem > 227 * 1024) {
     set_error("local join: shared memory %zu exceeds 227 KB (d=%d, H=%d)", smem, p.d, 1 << logH);
@@ -472,23 +779,55 @@ static int launch_join(const JoinParams &p, const int32_t *alist, const int32_t 
   return KNND_OK;
 }
 
-template <int G, bool GTAB>
-static int dispatch(const Plan &P, const JoinParams &p, const int32_t *alist, const int32_t *acount, int logH,
-                    int SW, int32_t *gslab, int64_t slab_ints, int grid_cap, cudaStream_t st) {
-#define KNND_NV(NV)                                                                                       \
-  case NV:                                                                                                \
-    return P.kpl == 1 ? launch_join<G, NV, 1, GTAB>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st) \
-                      : launch_join<G, NV, 2, GTAB>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st);
-  switch (p.ld == P.nv4 * 4 ? P.nv4 : 0) {
-    KNND_NV(2)
-    KNND_NV(3)
-    KNND_NV(5)
-    KNND_NV(13)
-    default:
-      return P.kpl == 1 ? launch_join<G, 0, 1, GTAB>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st)
-                        : launch_join<G, 0, 2, GTAB>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st);
+template <int NV4, int KPL>
+static int launch_warp(const JoinParams &p, const int32_t *alist, const int32_t *acount, int logH, int SW,
+                       cudaStream_t st) {
+  auto kern = join_warp_kernel<NV4, KPL>;
+  const WarpSlab L = warp_slab(p.d, p.ld, 1 << logH, SW);
+  const size_t smem = L.total * (WARP_BLOCK / 32);
+  if (smem > 227 * 1024) {
+    set_error("local join: warp slabs %zu B exceed 227 KB (d=%d, H=%d)", smem, p.d, 1 << logH);
+    return KNND_EUNSUPPORTED;
   }
-#undef KNND_NV
+  KNND_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  KNND_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARP_BLOCK, smem));
+  if (per_sm < 1) {
+    set_error("local join: warp kernel cannot be resident (smem=%zu)", smem);
+    return KNND_EUNSUPPORTED;
+  }
+  kern<<<per_sm * num_sms(), WARP_BLOCK, smem, st>>>(p, alist, acount, logH, SW);
+  KNND_LAUNCHED(1);
+  return KNND_OK;
+}
+
+// compile-time row widths (float4 count); anything else takes the generic path
+#define KNND_NV_SWITCH(CALL)            \
+  switch (p.ld == P.nv4 * 4 ? P.nv4 : 0) { \
+    case 2: CALL(2);                     \
+    case 3: CALL(3);                     \
+    case 5: CALL(5);                     \
+    case 13: CALL(13);                   \
+    default: CALL(0);                    \
+  }
+
+template <int G, bool GTAB>
+static int dispatch_block(const Plan &P, const JoinParams &p, const int32_t *alist, const int32_t *acount,
+                          int logH, int SW, int32_t *gslab, int64_t slab_ints, int grid_cap, cudaStream_t st) {
+#define KNND_CALL(NV)                                                                                          \
+  return P.kpl == 1 ? launch_join<G, NV, 1, GTAB>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st) \
+                    : launch_join<G, NV, 2, GTAB>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st)
+  KNND_NV_SWITCH(KNND_CALL)
+#undef KNND_CALL
+}
+
+static int dispatch_warp(const Plan &P, const JoinParams &p, const int32_t *alist, const int32_t *acount, int logH,
+                         int SW, cudaStream_t st) {
+#define KNND_CALL(NV)                                                      \
+  return P.kpl == 1 ? launch_warp<NV, 1>(p, alist, acount, logH, SW, st) \
+                    : launch_warp<NV, 2>(p, alist, acount, logH, SW, st)
+  KNND_NV_SWITCH(KNND_CALL)
+#undef KNND_CALL
 }
 
 }  // namespace knnd
@@ -560,21 +899,26 @@ int knnd_local_join(const double *points, const float *log32, const double *log6
   {
     int64_t blocks = (m + 255) / 256;
     if (blocks > (int64_t)num_sms() * 8) blocks = (int64_t)num_sms() * 8;
-    classify_kernel<<<(unsigned)blocks, 256, 0, st>>>(indptr, m, row_lo, k, P.PA, P.needB ? P.PB : P.PA,
-                                                      lists, counts);
+    classify_kernel<<<(unsigned)blocks, 256, 0, st>>>(indptr, m, row_lo, k, P.lim[0], P.lim[1], P.lim[2], lists,
+                                                      counts);
     KNND_LAUNCHED(1);
   }
   int rc;
-  if (P.needL) {
-    rc = dispatch<GL, true>(P, p, lists + 2 * m, counts + 2, P.logHL, P.swL, slabs, P.slab_ints, P.nslab, st);
+  if (P.need[3]) {
+    rc = dispatch_block<GL, true>(P, p, lists + 3 * m, counts + 3, P.logH[3], P.sw[3], slabs, P.slab_ints, P.nslab,
+                                  st);
     if (rc) return rc;
   }
-  rc = dispatch<GA, false>(P, p, lists, counts, P.logHA, P.swA, nullptr, 0, 0, st);
+  if (P.need[2]) {
+    rc = dispatch_block<GB, false>(P, p, lists + 2 * m, counts + 2, P.logH[2], P.sw[2], nullptr, 0, 0, st);
+    if (rc) return rc;
+  }
+  if (P.need[1]) {
+    rc = dispatch_warp(P, p, lists + m, counts + 1, P.logH[1], P.sw[1], st);
+    if (rc) return rc;
+  }
+  rc = dispatch_warp(P, p, lists, counts, P.logH[0], P.sw[0], st);
   if (rc) return rc;
-  if (P.needB) {
-    rc = dispatch<GB, false>(P, p, lists + m, counts + 1, P.logHB, P.swB, nullptr, 0, 0, st);
-    if (rc) return rc;
-  }
   return KNND_OK;
 }
 

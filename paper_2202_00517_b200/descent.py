@@ -320,24 +320,52 @@ def propose_new_friend_set(x: ItemId, state: KnnState, rs) -> np.ndarray:
     return out[0].cpu().numpy().astype(np.int64)
 
 
-def _run_rounds(dataset: Dataset, rs, cfg: DescentConfig, max_rounds: int, stop_on_fixed_point: bool):
-    n = len(dataset)
-    state = init_random_kout(dataset, rs, cfg, derive_rng(cfg.seed, STREAM_INIT))
-    tabs = device_tables_for(rs, state.device)
-    # every round's FCC sample is a function of (seed, round) only: draw them all up front
-    smp = np.stack([fcc_samples(n, cfg.k, cfg.fcc_sample_count, derive_rng(cfg.seed, STREAM_FCC, r))
-                    for r in range(1, max_rounds + 1)])
-    smp_dev = _to_device(smp, state.device)
+def draw_fcc_schedule(n: int, k: int, cfg: DescentConfig, max_rounds: int) -> np.ndarray:
+    """Every round's FCC sample is a function of (seed, round) only
+    (descent.py:305), so all of them are drawn up front: (R, 3, S) int32."""
+    return np.stack([fcc_samples(n, k, cfg.fcc_sample_count, derive_rng(cfg.seed, STREAM_FCC, r))
+                     for r in range(1, max_rounds + 1)])
+
+
+def descend_resident(eng: Engine, tabs, table: torch.Tensor, samples_dev: torch.Tensor, sample_count: int,
+                     max_rounds: int, stop_on_fixed_point: bool = False, on_round=None):
+    """The round loop of _run_rounds (descent.py:341-362) over device-resident
+    inputs: `table` holds the unsorted initial draws (own rows at least).
+    Sorts the initial rows (K6), then runs rounds until the FCC stalls (or no
+    row changes).  Returns (final KnnState, [RoundStats])."""
+    s = eng.shard
+    eng.ops.sort_rows(tabs, eng.own_rows(table), eng.k, s.lo, s.hi)
+    eng.exchange(table)
+    csr, mx = eng.build_csr(table)
+    state = KnnState._from_device(eng, table, csr, mx, 0, ())
     history: list[RoundStats] = []
     for r in range(1, max_rounds + 1):
         t0 = time.perf_counter()
-        state, res, rate = _round(state, tabs, smp_dev[r - 1], cfg.fcc_sample_count, r)
+        state, res, rate = _round(state, tabs, samples_dev[r - 1], sample_count, r)
         history.append(RoundStats(r, time.perf_counter() - t0, rate, res.comparisons, res.changed))
+        if on_round is not None:
+            on_round(state, history[-1])
         if stop_on_fixed_point:
             if res.changed == 0:
                 break
         elif len(history) >= 2 and history[-1].fcc <= history[-2].fcc:
             break
+    return state, history
+
+
+def _run_rounds(dataset: Dataset, rs, cfg: DescentConfig, max_rounds: int, stop_on_fixed_point: bool):
+    n = len(dataset)
+    k = cfg.k
+    if n <= k:
+        raise ConfigError(f"need n > k, got n={n}, k={k}")
+    tabs = device_tables_for(rs)
+    draws = random_kout_draws(n, k, derive_rng(cfg.seed, STREAM_INIT))
+    eng = Engine(n, k, tabs.device)
+    table = eng.alloc_table()
+    eng.upload_rows(draws, table)
+    smp_dev = _to_device(draw_fcc_schedule(n, k, cfg, max_rounds), tabs.device)
+    state, history = descend_resident(eng, tabs, table, smp_dev, cfg.fcc_sample_count, max_rounds,
+                                      stop_on_fixed_point)
     return state.friends, history
 
 

@@ -9,7 +9,8 @@ n, d, k = (int(a) for a in sys.argv[1:4])
 pts = port.experiment_points(n, d, 0)
 rs = b2.KlRankingSystem(pts, validate=False)
 cfg = b2.DescentConfig(k=k, seed=0)
-for rep in range(2):
+reps = int(sys.argv[4]) if len(sys.argv) > 4 else 2
+for rep in range(reps):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     st = b2.init_random_kout(b2.Dataset(pts), rs, cfg, b2.derive_rng(0, 2))
     torch.cuda.synchronize(); t1 = time.perf_counter()
