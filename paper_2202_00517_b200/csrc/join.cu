@@ -90,16 +90,29 @@ __device__ __forceinline__ void warp_append(bool take, int val, int *counter, in
 }
 
 // issue cp.async copies of the fp32 log rows of ids[0..nrow) into stage
-// (row stride ld floats), 16 B chunks, consecutive lanes on consecutive chunks
+// (row stride ld floats) in 16 B chunks: lane l copies chunk l % nv4 of rows
+// l / nv4, l / nv4 + 32 / nv4, ... so each warp instruction covers
+// floor(32 / nv4) whole rows (a few 128 B lines)
 template <int NV4>
 __device__ __forceinline__ void stage_rows_f32(float *stage, const float *__restrict__ log32, const int32_t *ids,
-                                               int nrow, int ld, int lane) {
-  const int nv4 = NV4 > 0 ? NV4 : (ld >> 2);
-  const int nchunk = nrow * nv4;
-  for (int c = lane; c < nchunk; c += 32) {
-    const int r = c / nv4, part = c - r * nv4;
-    const int y = ids[r];
-    cp_async16(stage + r * ld + part * 4, log32 + (int64_t)y * ld + part * 4);
+                                               int nrow, int ld_rt, int lane) {
+  const int ld = NV4 > 0 ? NV4 * 4 : ld_rt;
+  const int nv4 = ld >> 2;
+  if (nv4 <= 32) {
+    const int rpi = 32 / nv4;
+    const int r0 = lane / nv4, part = lane - r0 * nv4;
+    if (r0 < rpi) {
+      unsigned dst = smem_u32(stage) + (unsigned)(r0 * ld + part * 4) * 4u;
+      const unsigned dstep = (unsigned)(rpi * ld) * 4u;
+      const float *src = log32 + part * 4;
+      for (int r = r0; r < nrow; r += rpi, dst += dstep)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src + (int64_t)ids[r] * ld)
+                     : "memory");
+    }
+  } else {
+    for (int r = 0; r < nrow; ++r)
+      for (int part = lane; part < nv4; part += 32)
+        cp_async16(stage + r * ld + part * 4, log32 + (int64_t)ids[r] * ld + part * 4);
   }
 }
 
@@ -505,7 +518,7 @@ __global__ void __launch_bounds__(128) join_warp_kernel(JoinParams p, const int3
   extern __shared__ __align__(16) unsigned char sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int H = 1 << logH;
-  const unsigned shift = 32u - (unsigned)logH, hmask = (unsigned)H - 1u;
+  const unsigned shift = 32u - (unsigned)logH, bmask = ((unsigned)H >> 2) - 1u;
   const WarpSlab L = warp_slab(p.d, p.ld, H, SW);
   unsigned char *base = sm + (size_t)warp * L.total;
   float *x32 = reinterpret_cast<float *>(base + L.x32);
@@ -518,7 +531,7 @@ __global__ void __launch_bounds__(128) join_warp_kernel(JoinParams p, const int3
   double *stage64 = reinterpret_cast<double *>(table);         // phase 4: whole table
   const int K = p.K, K1 = K + 1;
   const int d = p.d, ld = p.ld, sd = d | 1;
-  const int rows = min(32, (2 * H) / (ld * 4));
+  const int rows = min(32, (H / 2) / (ld * 2));  // two staging buffers in the table's upper half
   const int rcap64 = min(32, (4 * H) / (sd * 8));
   const int Gq = 32 / K1, Gr = 32 % K1;
   const int s_init = lane / K1, j_init = lane % K1;
@@ -572,28 +585,27 @@ __global__ void __launch_bounds__(128) join_warp_kernel(JoinParams p, const int3
           const unsigned grp = __match_any_sync(FULL, valid ? y : -1 - lane);
           bool pending = valid && (__ffs(grp) - 1 == lane);
           bool isnew = false;
-          unsigned h = hash_slot(y, shift);
+          unsigned b = hash_slot(y, shift + 2);  // 4-slot bucket (one int4 read)
           while (__any_sync(FULL, pending)) {
-            bool claim = false;
+            int claim = -1;
             if (pending) {
-              const int cur = table[h];
-              if (cur == y) {
+              const int4 v = reinterpret_cast<const int4 *>(table)[b];
+              if (v.x == y || v.y == y || v.z == y || v.w == y) {
                 pending = false;
-              } else if (cur == EMPTY) {
-                claim = true;
-                table[h] = y;
               } else {
-                h = (h + 1) & hmask;
+                const int e = v.x == EMPTY ? 0 : v.y == EMPTY ? 1 : v.z == EMPTY ? 2 : v.w == EMPTY ? 3 : -1;
+                if (e >= 0) {
+                  claim = (int)(b * 4) + e;
+                  table[claim] = y;
+                } else {
+                  b = (b + 1) & bmask;
+                }
               }
             }
             __syncwarp();
-            if (claim) {
-              if (table[h] == y) {
-                pending = false;
-                isnew = true;
-              } else {
-                h = (h + 1) & hmask;
-              }
+            if (claim >= 0 && table[claim] == y) {  // a loser re-reads the same bucket
+              pending = false;
+              isnew = true;
             }
             __syncwarp();
           }
@@ -610,14 +622,24 @@ __global__ void __launch_bounds__(128) join_warp_kernel(JoinParams p, const int3
 #pragma unroll
     for (int q = 0; q < Q; ++q) best[q] = __int_as_float(0x7f800000);
     float am = 0.f;
-    for (int k0 = 0; k0 < U; k0 += rows) {
+    if (U > 0) {
+      stage_rows_f32<NV4>(stage, p.log32, list, min(rows, U), ld, lane);
+      cp_async_commit();
+    }
+    for (int k0 = 0, buf = 0; k0 < U; k0 += rows, buf ^= 1) {
       const int nrow = min(rows, U - k0);
-      stage_rows_f32<NV4>(stage, p.log32, list + k0, nrow, ld, lane);
-      cp_async_wait_all();
+      if (k0 + rows < U) {  // prefetch the next batch into the other buffer
+        stage_rows_f32<NV4>(stage + (buf ^ 1) * rows * ld, p.log32, list + k0 + rows, min(rows, U - k0 - rows), ld,
+                            lane);
+        cp_async_commit();
+        cp_async_wait_1();
+      } else {
+        cp_async_wait_0();
+      }
       __syncwarp();
       if (lane < nrow) {
         float ce, ab;
-        screen_row<NV4>(stage + lane * ld, x32, ld, ce, ab);
+        screen_row<NV4>(stage + buf * rows * ld + lane * ld, x32, ld, ce, ab);
         scores[k0 + lane] = ce;
         am = fmaxf(am, ab);
         float v = ce;
