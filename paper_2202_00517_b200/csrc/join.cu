@@ -30,6 +30,9 @@
 //   W1, W2  one warp per anchor, private smem slab (table of H1 / 2*H1 slots)
 //   B       one 256-thread block per anchor, table of up to 2^15 slots in smem
 //   L       one 512-thread block per anchor, table in a global-memory slab
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 #include "score.cuh"
 
@@ -305,7 +308,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     S = slab;
     table = slab + SW;
     list = table + H;
-    wrows = LSTAGE_ROWS;
+    wrows = LSTAGE_ROWS / 2;  // two buffers per warp
     wstage = reinterpret_cast<float *>(sm + L.stage) + (size_t)warp * LSTAGE_ROWS * p.ld;
     stage64 = reinterpret_cast<double *>(sm + L.stage);
     rcap64 = 32;
@@ -314,7 +317,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     table = reinterpret_cast<int32_t *>(sm + L.table);
     list = reinterpret_cast<int32_t *>(sm + L.list);
     const int per_warp_floats = (H / 2) / W;  // upper half of the table, split over warps
-    wrows = min(32, per_warp_floats / p.ld);
+    wrows = min(32, per_warp_floats / (2 * p.ld));  // two buffers per warp
     wstage = reinterpret_cast<float *>(table + H / 2) + (size_t)warp * per_warp_floats;
     stage64 = reinterpret_cast<double *>(table);  // lower half, free in phase 4
     rcap64 = min(32, (2 * H) / ((p.d | 1) * 8));
@@ -385,14 +388,24 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     // ---- phase 2: fp32 screen, one staged batch of rows per warp at a time
     float *scores = reinterpret_cast<float *>(table);  // the hash table is dead now
     float mn = __int_as_float(0x7f800000), mx = -mn, am = 0.f;
-    for (int k0 = warp * wrows; k0 < U; k0 += W * wrows) {
+    if (warp * wrows < U) {
+      stage_rows_f32<NV4>(wstage, p.log32, list + warp * wrows, min(wrows, U - warp * wrows), ld, lane);
+      cp_async_commit();
+    }
+    for (int k0 = warp * wrows, buf = 0; k0 < U; k0 += W * wrows, buf ^= 1) {
       const int nrow = min(wrows, U - k0);
-      stage_rows_f32<NV4>(wstage, p.log32, list + k0, nrow, ld, lane);
-      cp_async_wait_all();
+      const int k1 = k0 + W * wrows;
+      if (k1 < U) {  // prefetch this warp's next batch into the other buffer
+        stage_rows_f32<NV4>(wstage + (buf ^ 1) * wrows * ld, p.log32, list + k1, min(wrows, U - k1), ld, lane);
+        cp_async_commit();
+        cp_async_wait_1();
+      } else {
+        cp_async_wait_0();
+      }
       __syncwarp();
       if (lane < nrow) {
         float ce, ab;
-        screen_row<NV4>(wstage + lane * ld, x32, ld, ce, ab);
+        screen_row<NV4>(wstage + buf * wrows * ld + lane * ld, x32, ld, ce, ab);
         scores[k0 + lane] = ce;
         mn = fminf(mn, ce);
         mx = fmaxf(mx, ce);
@@ -512,7 +525,7 @@ __host__ __device__ inline WarpSlab warp_slab(int d, int ld, int H, int SW) {
 }
 
 template <int NV4, int KPL>
-__global__ void __launch_bounds__(128) join_warp_kernel(JoinParams p, const int32_t *__restrict__ alist,
+__global__ void __launch_bounds__(128, 4) join_warp_kernel(JoinParams p, const int32_t *__restrict__ alist,
                                                         const int32_t *__restrict__ acount, int logH, int SW) {
   constexpr int Q = 2 * KPL;  // per-lane kept screened values
   extern __shared__ __align__(16) unsigned char sm[];
@@ -561,15 +574,15 @@ __global__ void __launch_bounds__(128) join_warp_kernel(JoinParams p, const int3
     int U = 0;
     {
       int s = s_init, j = j_init;
-      for (int e0 = 0; e0 < total; e0 += 32 * UNR1) {
-        int id[UNR1];
+      int nxt[UNR1];  // the next group of pre-dedup ids, loaded one group ahead
+      auto load_group = [&](int e0) {
 #pragma unroll
         for (int u = 0; u < UNR1; ++u) {
           const int e = e0 + u * 32 + lane;
-          id[u] = -1;
+          nxt[u] = -1;
           if (e < total) {
             const int v = S[s];
-            id[u] = (j == 0) ? v : __ldg(p.F + (int64_t)v * K + (j - 1));
+            nxt[u] = (j == 0) ? v : __ldg(p.F + (int64_t)v * K + (j - 1));
           }
           s += Gq;
           j += Gr;
@@ -578,6 +591,13 @@ __global__ void __launch_bounds__(128) join_warp_kernel(JoinParams p, const int3
             ++s;
           }
         }
+      };
+      load_group(0);
+      for (int e0 = 0; e0 < total; e0 += 32 * UNR1) {
+        int id[UNR1];
+#pragma unroll
+        for (int u = 0; u < UNR1; ++u) id[u] = nxt[u];
+        if (e0 + 32 * UNR1 < total) load_group(e0 + 32 * UNR1);
 #pragma unroll
         for (int u = 0; u < UNR1; ++u) {
           const int y = id[u];
@@ -695,11 +715,16 @@ __global__ void __launch_bounds__(128) join_warp_kernel(JoinParams p, const int3
   }
 }
 
-// bin the anchors of [lo, hi) by pre-dedup bound P = (K+c)(K+1):
-// class 0: P <= lim[0], class 1: P <= lim[1], class 2: P <= lim[2], class 3: rest
-__global__ void classify_kernel(const int64_t *__restrict__ indptr, int64_t m, int64_t lo, int K, int64_t lim0,
-                                int64_t lim1, int64_t lim2, int32_t *__restrict__ lists,
-                                int32_t *__restrict__ counts) {
+// bin the anchors of [lo, hi) by pre-dedup bound P = (K+c)(K+1): class i is
+// the first with P <= lim[i]; the last class (global-memory tables) takes the rest
+constexpr int MAXCLS = 5;
+struct Lims {
+  int64_t v[MAXCLS];
+  int n;  // number of classes (the last one is unbounded)
+};
+
+__global__ void classify_kernel(const int64_t *__restrict__ indptr, int64_t m, int64_t lo, int K, Lims lims,
+                                int32_t *__restrict__ lists, int32_t *__restrict__ counts) {
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < m; base += stride) {
@@ -708,29 +733,34 @@ __global__ void classify_kernel(const int64_t *__restrict__ indptr, int64_t m, i
     if (xr < m) {
       const int64_t c = indptr[xr + 1] - indptr[xr];
       const int64_t P = ((int64_t)K + c) * (K + 1);
-      cls = P <= lim0 ? 0 : (P <= lim1 ? 1 : (P <= lim2 ? 2 : 3));
+      cls = lims.n - 1;
+      for (int i = lims.n - 2; i >= 0; --i)
+        if (P <= lims.v[i]) cls = i;
     }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) warp_append(cls == k, (int)(lo + xr), counts + k, lists + (int64_t)k * m, lane);
+    for (int k = 0; k < lims.n; ++k) warp_append(cls == k, (int)(lo + xr), counts + k, lists + (int64_t)k * m, lane);
   }
 }
 
 // ---------------------------------------------------------------------------
-// host side
+// host side: the size-class plan
 
-// size classes: W1, W2 warp-per-anchor; B block (shared table); L block (global table)
+enum { KIND_WARP = 0, KIND_BLOCK128 = 1, KIND_BLOCK256 = 2, KIND_GLOBAL = 3 };
+
+struct Cls {
+  int kind, logH, sw;
+  int64_t lim;  // pre-dedup bound handled (H/2 for shared-memory tables)
+  bool need;
+};
+
 struct Plan {
-  int kpl, nv4;
-  int logH[4];
-  int sw[4];
-  int64_t lim[3];
-  bool need[4];
+  int kpl, nv4, ncls;
+  Cls c[MAXCLS];
   int nslab;
   int64_t slab_ints;
   size_t lists_off, counts_off, slab_off, total;
 };
 
-constexpr int WARP_BLOCK = 128, GB = 256, GL = 512;
+constexpr int WARP_BLOCK = 128, GL = 512;
 
 static int ilog2_ceil(int64_t v) {
   int l = 0;
@@ -738,37 +768,87 @@ static int ilog2_ceil(int64_t v) {
   return l;
 }
 
+// KNND_PLAN overrides the shared-memory classes, e.g. "w11,b128:12,b256:14"
+// (w = warp per anchor, bG = G-thread block per anchor, :L = log2 table slots)
+static int parse_plan(const char *spec, int kind[], int logH[]) {
+  int n = 0;
+  const char *q = spec;
+  while (*q && n < MAXCLS - 1) {
+    int k, l = 0;
+    if (q[0] == 'w') {
+      k = KIND_WARP;
+      l = atoi(q + 1);
+    } else if (q[0] == 'b' && !strncmp(q + 1, "128:", 4)) {
+      k = KIND_BLOCK128;
+      l = atoi(q + 5);
+    } else if (q[0] == 'b' && !strncmp(q + 1, "256:", 4)) {
+      k = KIND_BLOCK256;
+      l = atoi(q + 5);
+    } else {
+      return 0;
+    }
+    if (l < 8 || l > 15) return 0;
+    kind[n] = k;
+    logH[n] = l;
+    ++n;
+    q = strchr(q, ',');
+    if (!q) break;
+    ++q;
+  }
+  return n;
+}
+
 static Plan make_plan(int64_t m, int d, int K, int max_indeg) {
   Plan P{};
   P.kpl = K <= 32 ? 1 : 2;
   P.nv4 = (d + 3) / 4;
   const int64_t K1 = K + 1;
-  // W1 holds in-degrees up to ~1.4K (the bulk of a random K-out graph), W2 twice
-  // that; B (one block, shared table <= 2^15 slots) the tail; L the hubs.
+  const int ld = (d + 3) / 4 * 4;
+  // default: warp per anchor for in-degrees up to ~1.4K (the bulk of a random
+  // K-out graph), 128-thread blocks up to ~2.3x that, 256-thread blocks for the
+  // tail, global tables for the hubs
   int l1 = ilog2_ceil(2 * K1 * (K + (2 * K) / 5));
-  const int lstage = ilog2_ceil(64 * (int64_t)((d + 3) / 4 * 4));  // 32 staged fp32 rows fit in H/2 slots
+  const int lstage = ilog2_ceil(64 * (int64_t)ld);  // 32 staged fp32 rows fit in H/2 slots
   if (l1 < lstage) l1 = lstage;
   if (l1 < 9) l1 = 9;
   if (l1 > 12) l1 = 12;
-  P.logH[0] = l1;
-  P.logH[1] = l1 + 1;
-  P.logH[2] = l1 + 3 < 15 ? l1 + 3 : 15;
-  for (int i = 0; i < 3; ++i) {
-    P.lim[i] = ((int64_t)1 << P.logH[i]) / 2;
-    P.sw[i] = (int)(P.lim[i] / K1 + 1);
+  int kind[MAXCLS] = {KIND_WARP, KIND_BLOCK128, KIND_BLOCK256};
+  int logH[MAXCLS] = {l1, l1 + 1, l1 + 3 < 15 ? l1 + 3 : 15};
+  int n = 3;
+  if (const char *env = getenv("KNND_PLAN")) {
+    int k2[MAXCLS], l2[MAXCLS];
+    const int n2 = parse_plan(env, k2, l2);
+    if (n2 > 0) {
+      n = n2;
+      for (int i = 0; i < n; ++i) {
+        kind[i] = k2[i];
+        logH[i] = l2[i];
+      }
+    }
   }
   const int64_t Pmax = ((int64_t)K + max_indeg) * K1;
-  P.need[0] = true;
-  P.need[1] = Pmax > P.lim[0];
-  P.need[2] = Pmax > P.lim[1];
-  P.need[3] = Pmax > P.lim[2];
-  P.logH[3] = P.need[3] ? ilog2_ceil(2 * Pmax) : 0;
-  P.sw[3] = (K + max_indeg + 31) & ~31;  // keeps the table int4-aligned in the slab
-  P.nslab = P.need[3] ? 2 * num_sms() : 0;
-  P.slab_ints = P.need[3] ? (int64_t)align_up((size_t)P.sw[3] + ((size_t)3 << P.logH[3]) / 2, 64) : 0;
+  int64_t prev = 0;
+  for (int i = 0; i < n; ++i) {
+    Cls &c = P.c[i];
+    c.kind = kind[i];
+    c.logH = logH[i];
+    c.lim = ((int64_t)1 << c.logH) / 2;
+    c.sw = (int)(c.lim / K1 + 1);
+    c.need = i == 0 || Pmax > prev;
+    prev = c.lim;
+  }
+  Cls &g = P.c[n];
+  g.kind = KIND_GLOBAL;
+  g.need = Pmax > prev;
+  g.lim = INT64_MAX;
+  g.logH = g.need ? ilog2_ceil(2 * Pmax) : 0;
+  g.sw = (K + max_indeg + 31) & ~31;  // keeps the table int4-aligned in the slab
+  P.ncls = n + 1;
+  P.nslab = g.need ? 2 * num_sms() : 0;
+  P.slab_ints = g.need ? (int64_t)align_up((size_t)g.sw + ((size_t)3 << g.logH) / 2, 64) : 0;
   size_t o = 0;
   P.lists_off = o;
-  o = align_up(o + (size_t)4 * m * 4, 256);
+  o = align_up(o + (size_t)P.ncls * m * 4, 256);
   P.counts_off = o;
   o = align_up(o + 64, 256);
   P.slab_off = o;
@@ -824,13 +904,13 @@ static int launch_warp(const JoinParams &p, const int32_t *alist, const int32_t 
 }
 
 // compile-time row widths (float4 count); anything else takes the generic path
-#define KNND_NV_SWITCH(CALL)            \
+#define KNND_NV_SWITCH(CALL)               \
   switch (p.ld == P.nv4 * 4 ? P.nv4 : 0) { \
-    case 2: CALL(2);                     \
-    case 3: CALL(3);                     \
-    case 5: CALL(5);                     \
-    case 13: CALL(13);                   \
-    default: CALL(0);                    \
+    case 2: CALL(2);                       \
+    case 3: CALL(3);                       \
+    case 5: CALL(5);                       \
+    case 13: CALL(13);                     \
+    default: CALL(0);                      \
   }
 
 template <int G, bool GTAB>
@@ -850,6 +930,23 @@ static int dispatch_warp(const Plan &P, const JoinParams &p, const int32_t *alis
                     : launch_warp<NV, 2>(p, alist, acount, logH, SW, st)
   KNND_NV_SWITCH(KNND_CALL)
 #undef KNND_CALL
+}
+
+static int dispatch_class(const Plan &P, int i, const JoinParams &p, const int32_t *lists, const int32_t *counts,
+                          int64_t m, int32_t *slabs, cudaStream_t st) {
+  const Cls &c = P.c[i];
+  const int32_t *alist = lists + (int64_t)i * m;
+  const int32_t *acount = counts + i;
+  switch (c.kind) {
+    case KIND_WARP:
+      return dispatch_warp(P, p, alist, acount, c.logH, c.sw, st);
+    case KIND_BLOCK128:
+      return dispatch_block<128, false>(P, p, alist, acount, c.logH, c.sw, nullptr, 0, 0, st);
+    case KIND_BLOCK256:
+      return dispatch_block<256, false>(P, p, alist, acount, c.logH, c.sw, nullptr, 0, 0, st);
+    default:
+      return dispatch_block<GL, true>(P, p, alist, acount, c.logH, c.sw, slabs, P.slab_ints, P.nslab, st);
+  }
 }
 
 }  // namespace knnd
@@ -919,28 +1016,20 @@ int knnd_local_join(const double *points, const float *log32, const double *log6
 
   KNND_CUDA(cudaMemsetAsync(counts, 0, 64, st));
   {
+    Lims lims;
+    lims.n = P.ncls;
+    for (int i = 0; i < P.ncls; ++i) lims.v[i] = P.c[i].lim;
     int64_t blocks = (m + 255) / 256;
     if (blocks > (int64_t)num_sms() * 8) blocks = (int64_t)num_sms() * 8;
-    classify_kernel<<<(unsigned)blocks, 256, 0, st>>>(indptr, m, row_lo, k, P.lim[0], P.lim[1], P.lim[2], lists,
-                                                      counts);
+    classify_kernel<<<(unsigned)blocks, 256, 0, st>>>(indptr, m, row_lo, k, lims, lists, counts);
     KNND_LAUNCHED(1);
   }
-  int rc;
-  if (P.need[3]) {
-    rc = dispatch_block<GL, true>(P, p, lists + 3 * m, counts + 3, P.logH[3], P.sw[3], slabs, P.slab_ints, P.nslab,
-                                  st);
+  // biggest tables first: the few long hub anchors start early
+  for (int i = P.ncls - 1; i >= 0; --i) {
+    if (!P.c[i].need) continue;
+    const int rc = dispatch_class(P, i, p, lists, counts, m, slabs, st);
     if (rc) return rc;
   }
-  if (P.need[2]) {
-    rc = dispatch_block<GB, false>(P, p, lists + 2 * m, counts + 2, P.logH[2], P.sw[2], nullptr, 0, 0, st);
-    if (rc) return rc;
-  }
-  if (P.need[1]) {
-    rc = dispatch_warp(P, p, lists + m, counts + 1, P.logH[1], P.sw[1], st);
-    if (rc) return rc;
-  }
-  rc = dispatch_warp(P, p, lists, counts, P.logH[0], P.sw[0], st);
-  if (rc) return rc;
   return KNND_OK;
 }
 
