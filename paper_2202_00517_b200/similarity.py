@@ -57,6 +57,8 @@ def _stream(device: torch.device) -> int:
 
 
 def _dev(device) -> torch.device:
+    if device is None and not torch.cuda.is_available():
+        raise RuntimeError("no CUDA device: the B200 KL local join has no CPU fallback")
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     if dev.type != "cuda":
         raise RuntimeError(f"the KL local join runs on CUDA devices only, got {dev}")

@@ -1,0 +1,127 @@
+"""Host-side logic of the drop-in API (no GPU): config validation, budgets,
+RNG substreams and the host draws, which must consume the reference's numpy
+streams exactly (checked against the oracle port and the golden fixtures)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2202_00517_b200 as b2
+from oracle import port
+from paper_2202_00517_b200.engine import Shard
+from parity import sha_i32
+
+
+def test_round_budget_table(known):
+    for n, k, b in known["round_budget"]:
+        assert b2.round_budget(n, k) == b
+    assert b2.round_budget(256, 16) == 4 and b2.round_budget(16, 16) == 2
+    with pytest.raises(b2.ConfigError):
+        b2.round_budget(1, 16)
+    with pytest.raises(b2.ConfigError):
+        b2.round_budget(100, 1)
+
+
+def test_descent_config_validation():
+    cfg = b2.DescentConfig(k=16)
+    assert cfg.fcc_sample_count == 1000 and cfg.resolved_workers() == 1
+    assert cfg.resolved_max_rounds(20_000) == b2.round_budget(20_000, 16) + 4
+    assert b2.DescentConfig(k=4, max_rounds=3).resolved_max_rounds(10_000) == 3
+    assert b2.DescentConfig(k=4, worker_count="auto").resolved_workers() >= 1
+    for bad in (dict(k=1), dict(k=4, fcc_sample_count=0), dict(k=4, max_rounds=0), dict(k=4, worker_count=0),
+                dict(k=4, worker_count="many")):
+        with pytest.raises(b2.ConfigError):
+            b2.DescentConfig(**bad)
+    assert issubclass(b2.ConfigError, ValueError)
+
+
+def test_dataset_and_ranking_validation():
+    with pytest.raises(b2.ConfigError):
+        b2.Dataset(np.zeros((1, 3)))
+    with pytest.raises(ValueError):
+        b2.KlRankingSystem(np.array([[0.6, 0.6]]))
+    with pytest.raises(ValueError):
+        b2.KlRankingSystem(np.array([[0.5, 0.0, 0.5]]))
+    b2.KlRankingSystem(np.array([[0.6, 0.6]]), validate=False)
+    with pytest.raises(ValueError):
+        b2.sample_simplex_uniform(1, 10, 0)
+    with pytest.raises(ValueError):
+        b2.sample_simplex_uniform(3, 0, 0)
+
+
+def test_derive_rng_substreams():
+    a = b2.derive_rng(5, 3, 1).integers(0, 1 << 32, 8)
+    assert np.array_equal(a, b2.derive_rng(5, 3, 1).integers(0, 1 << 32, 8))
+    assert not np.array_equal(a, b2.derive_rng(5, 3, 2).integers(0, 1 << 32, 8))
+    assert not np.array_equal(a, b2.derive_rng(6, 3, 1).integers(0, 1 << 32, 8))
+    assert b2.derive_rng(-1, 2).integers(0, 10) in range(10)
+    assert np.array_equal(b2.derive_rng(7, 1, 20).integers(0, 99, 5), port.substream(7, 1, 20).integers(0, 99, 5))
+
+
+@pytest.mark.parametrize("n,d,seed", [(300, 6, 3), (2000, 20, 0), (100_000, 10, 0)])
+def test_points_generator_matches_reference_stream(n, d, seed):
+    a = b2.sample_simplex_uniform(d, n, b2.derive_rng(seed, b2.STREAM_DATA, d))
+    assert np.array_equal(a, port.experiment_points(n, d, seed))
+
+
+@pytest.mark.parametrize("n,k", [(300, 7), (5, 4), (12, 6), (800, 40), (100_000, 20), (20_000, 3)])
+def test_random_kout_draws_consume_the_reference_stream(n, k):
+    a = b2.random_kout_draws(n, k, b2.derive_rng(11, 2))
+    b = port.random_kout_draws(n, k, port.substream(11, 2))
+    assert np.array_equal(a, b)
+    anchors = np.arange(n)[:, None]
+    assert not (a == anchors).any()
+    s = np.sort(a, axis=1)
+    assert not (s[:, 1:] == s[:, :-1]).any()
+
+
+def test_rejection_redraws_are_exercised():
+    # n - 1 > 2K^2 but small enough that first draws collide in some rows
+    n, k = 60, 5
+    rng = b2.derive_rng(3, 2)
+    first = rng.integers(0, n - 1, size=(n, k), dtype=np.int64)
+    first += first >= np.arange(n)[:, None]
+    s = np.sort(first, axis=1)
+    assert (s[:, 1:] == s[:, :-1]).any(), "the seed must produce at least one redraw"
+    assert np.array_equal(b2.random_kout_draws(n, k, b2.derive_rng(3, 2)), port.random_kout_draws(n, k, port.substream(3, 2)))
+
+
+@pytest.mark.parametrize("r", [1, 2, 7])
+def test_fcc_samples_match_reference_stream(r):
+    got = b2.fcc_samples(1000, 20, 1000, b2.derive_rng(0, 3, r))
+    xs, i, j = port.fcc_draws(1000, 20, 1000, port.substream(0, 3, r))
+    assert np.array_equal(got, np.stack([xs, i, j]).astype(np.int32))
+    assert (got[1] != got[2]).all()
+
+
+def test_fcc_schedule_is_round_indexed():
+    cfg = b2.DescentConfig(k=10, seed=4)
+    from paper_2202_00517_b200.descent import draw_fcc_schedule
+
+    sched = draw_fcc_schedule(5000, 10, cfg, 6)
+    for r in range(1, 7):
+        assert np.array_equal(sched[r - 1], b2.fcc_samples(5000, 10, 1000, b2.derive_rng(4, 3, r)))
+
+
+@pytest.mark.parametrize("n,world", [(10, 1), (10, 3), (1_000_000, 8), (7, 8), (100_001, 2)])
+def test_shards_cover_rows_once(n, world):
+    shards = [Shard(r, world, n) for r in range(world)]
+    covered = np.zeros(n, dtype=int)
+    for s in shards:
+        assert s.padded_rows >= n and s.padded_rows == s.chunk * world
+        covered[s.lo:s.hi] += 1
+        assert s.hi - s.lo <= s.chunk
+    assert (covered == 1).all()
+
+
+def test_golden_init_is_reachable_from_host_draws(small_meta, small_tables):
+    """The host draws + the oracle row sort reproduce the reference's initial table,
+    so the device only has to reproduce the row sort."""
+    from oracle import native
+
+    for name in ("n300_d6_k7_s3", "n1000_d20_k20_s1"):
+        meta = small_meta[name]
+        pts = b2.sample_simplex_uniform(meta["d"], meta["n"], b2.derive_rng(meta["seed"], 1, meta["d"]))
+        draws = b2.random_kout_draws(meta["n"], meta["k"], b2.derive_rng(meta["seed"], 2))
+        assert sha_i32(native.sort_rows(native.Tables(pts), draws)) == meta["init_sha"]
