@@ -19,8 +19,8 @@ are input generation here and are timed in `e2e`.
              4*d per comparison (the fp32 log row of each unique candidate)
              / its CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs
   cpu_baseline  the C oracle (oracle/knnd_oracle.c, all host threads) on a
-             bounded sample of the same workload: the round-1 local join of
-             200,000 sampled anchors
+             bounded sample of the same workload: the full round-1 local join
+             (all anchors of the round-1 input table)
 
 `--impl reference` times that CPU implementation alone (rank 0 only).
 """
@@ -49,7 +49,7 @@ CONFIGS = {
     "c4": (1_000_000, 50, 30),
     "c5": (10_000_000, 20, 20),
 }
-CPU_SAMPLE_ANCHORS = 200_000
+CPU_SAMPLE_ANCHORS = 10_000_000  # i.e. every anchor of round 1 (bounded by n)
 
 
 def parse():
@@ -139,7 +139,8 @@ def cpu_sample_setup(n, d, k, seed, anchors=CPU_SAMPLE_ANCHORS):
     tab = native.Tables(pts)
     init = native.sort_rows(tab, port.random_kout_draws(n, k, port.substream(seed, port.TAG_INIT)))
     csr = native.transpose(init)
-    sample = np.sort(np.random.default_rng(seed).choice(n, size=min(anchors, n), replace=False))
+    sample = (np.arange(n, dtype=np.int64) if anchors >= n
+              else np.sort(np.random.default_rng(seed).choice(n, size=anchors, replace=False)))
     return tab, init, csr, sample
 
 
@@ -170,7 +171,7 @@ def reference_arm(args):
         secs += s
     v = comps / secs
     cores = cpu_threads()
-    sample_desc = (f"round-1 local join (descent.py:230-242) of {sample.size} uniformly sampled anchors of "
+    sample_desc = (f"round-1 local join (descent.py:230-242) of {sample.size} anchors of "
                    f"{args.config.upper()} via the C oracle, {cores} OpenMP threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
@@ -311,7 +312,7 @@ def b200_arm(args):
         c, s_ = cpu_sample_run(tab, init, csr, sample)
         cores = cpu_threads()
         cpu = {"value": c / s_, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"round-1 local join of {sample.size} sampled anchors of {args.config.upper()}, "
+               "sample": f"round-1 local join of {sample.size} anchors of {args.config.upper()}, "
                          f"C oracle (oracle/knnd_oracle.c), {cores} threads, {s_:.2f} s"}
 
     if rank == 0:

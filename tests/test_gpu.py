@@ -259,18 +259,38 @@ def _trajectory_check(traj, name, tie_check_threads=0):
         if len(hist) >= 2 and hist[-1].fcc <= hist[-2].fcc:
             break
     assert len(hist) == len(ref["rounds"])
+    return pts, st.friends
+
+
+def _recall_check(name, pts, final, golden, size):
+    """recall@K (evaluation.py:111-132) on the reference's recall sample vs the
+    recorded reference value on the same queries (BASELINE: within 0.005)."""
+    n, k = final.shape
+    q = np.arange(n) if size is None else port.recall_sample(n, 0, size)[:2000]
+    exact = native.exact_rows(native.Tables(pts), q, k)
+    rec = port.recall_of(final, exact, q)
+    ref = golden[name]["recall" if size is None else "recall_first2000"]
+    assert abs(rec - ref) <= 0.005, (rec, ref)
+    return rec
 
 
 def test_c1_trajectory(cuda, trajectories):
-    _trajectory_check(trajectories, "c1")
+    from conftest import load_json
+
+    pts, final = _trajectory_check(trajectories, "c1")
+    _recall_check("c1", pts, final, load_json("recall.json"), None)
 
 
 def test_c2_trajectory(cuda, trajectories):
-    _trajectory_check(trajectories, "c2")
+    from conftest import load_json
+
+    pts, final = _trajectory_check(trajectories, "c2")
+    _recall_check("c2", pts, final, load_json("recall.json"), 10_000)
 
 
 @pytest.mark.slow
 def test_c3_trajectory(cuda, trajectories):
-    if "c3" not in trajectories or "rounds_used" not in trajectories["c3"]:
-        pytest.skip("reference C3 trajectory not recorded yet")
-    _trajectory_check(trajectories, "c3")
+    from conftest import load_json
+
+    pts, final = _trajectory_check(trajectories, "c3")
+    _recall_check("c3", pts, final, load_json("recall.json"), 10_000)
