@@ -95,7 +95,12 @@ int knnd_csr_build(const int32_t *friends, int64_t n, int32_t k, int64_t row_lo,
  *   tally[2] += #anchors with |U_x| < K (malformed input; must stay 0)
  *   (tally is 4 x uint64, device memory, accumulated — the caller zeroes it)
  * max_indeg must be >= the longest CSR segment (from knnd_csr_build).
+ * flags: KNND_JOIN_NONPOS_LOG when every coordinate of every point is <= 1
+ * (all logs <= 0, e.g. simplex data): the screen's error scale
+ * sum |x log y| then equals -sum x log y and is not accumulated separately.
+ * Results do not depend on flags (only the work does).
  */
+#define KNND_JOIN_NONPOS_LOG 1u
 size_t knnd_local_join_workspace_bytes(int64_t n, int32_t d, int32_t k, int64_t row_lo,
                                        int64_t row_hi, int32_t max_indeg);
 int knnd_local_join(const double *points, const float *log32, const double *log64,
@@ -104,7 +109,7 @@ int knnd_local_join(const double *points, const float *log32, const double *log6
                     const int32_t *indices, int64_t row_lo, int64_t row_hi,
                     int32_t max_indeg, int32_t *out_ids, double *out_kl,
                     int32_t *out_ucount, unsigned long long *tally, void *ws,
-                    size_t ws_bytes, void *stream);
+                    size_t ws_bytes, uint32_t flags, void *stream);
 
 /*
  * Friend clustering rate count — friend_clustering_rate (descent.py:317-338)

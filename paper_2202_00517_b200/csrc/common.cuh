@@ -126,6 +126,12 @@ struct WarpTopK {
     if (KPL > 1 && i >= 32) r = b[KPL - 1];
     return r.shfl(i & 31);
   }
+  // the first batch into an empty buffer: just sort it
+  __device__ __forceinline__ void first(Key v, int lane) {
+    b[0] = warp_sort32(v, lane);
+#pragma unroll
+    for (int q = 1; q < KPL; ++q) b[q] = Key::inf();
+  }
   // insert one candidate per lane (pass Key::inf() for "none")
   __device__ __forceinline__ void insert(Key v, int K, int lane) {
     Key kth = get(K - 1);

@@ -56,6 +56,7 @@ struct JoinParams {
   int64_t lo;
   int d, ld, K;
   float band;
+  int nonpos;  // every log coordinate <= 0: sum |x log y| == -sum x log y exactly
 };
 
 __host__ __device__ inline size_t al16(size_t v) { return (v + 15) & ~(size_t)15; }
@@ -119,13 +120,31 @@ __device__ __forceinline__ void stage_rows_f32(float *stage, const float *__rest
   }
 }
 
-// ce = -sum x*l and ab = sum |x*l| of one staged row (left to right)
+// ce = -sum x*l and ab = sum |x*l| of one staged row (left to right).  With
+// nonpos (all logs <= 0) every term of ab equals the term of ce, so ab == ce
+// bit for bit and only one accumulator is needed.
 template <int NV4>
-__device__ __forceinline__ void screen_row(const float *row, const float *x32, int ld, float &ce, float &ab) {
+__device__ __forceinline__ void screen_row(const float *row, const float *x32, int ld, int nonpos, float &ce,
+                                           float &ab) {
   const float4 *r4 = reinterpret_cast<const float4 *>(row);
   const float4 *x4 = reinterpret_cast<const float4 *>(x32);
   const int nv4 = NV4 > 0 ? NV4 : (ld >> 2);
   float a = 0.f, b = 0.f;
+  if (nonpos) {
+#pragma unroll
+    for (int q = 0; q < (NV4 > 0 ? NV4 : 64); ++q) {
+      if (NV4 == 0 && q >= nv4) break;
+      const float4 xv = x4[q];
+      const float4 l = r4[q];
+      a = fmaf(-xv.x, l.x, a);
+      a = fmaf(-xv.y, l.y, a);
+      a = fmaf(-xv.z, l.z, a);
+      a = fmaf(-xv.w, l.w, a);
+    }
+    ce = a;
+    ab = a;
+    return;
+  }
 #pragma unroll
   for (int q = 0; q < (NV4 > 0 ? NV4 : 64); ++q) {
     if (NV4 == 0 && q >= nv4) break;
@@ -139,6 +158,41 @@ __device__ __forceinline__ void screen_row(const float *row, const float *x32, i
     b = fmaf(xv.y, fabsf(l.y), b);
     b = fmaf(xv.z, fabsf(l.z), b);
     b = fmaf(xv.w, fabsf(l.w), b);
+  }
+  ce = a;
+  ab = b;
+}
+
+// same with the anchor row held in registers (warp kernel, compile-time width)
+template <int NV4>
+__device__ __forceinline__ void screen_row_reg(const float *row, const float4 (&xr)[NV4], int nonpos, float &ce,
+                                               float &ab) {
+  const float4 *r4 = reinterpret_cast<const float4 *>(row);
+  float a = 0.f, b = 0.f;
+  if (nonpos) {
+#pragma unroll
+    for (int q = 0; q < NV4; ++q) {
+      const float4 l = r4[q];
+      a = fmaf(-xr[q].x, l.x, a);
+      a = fmaf(-xr[q].y, l.y, a);
+      a = fmaf(-xr[q].z, l.z, a);
+      a = fmaf(-xr[q].w, l.w, a);
+    }
+    ce = a;
+    ab = a;
+    return;
+  }
+#pragma unroll
+  for (int q = 0; q < NV4; ++q) {
+    const float4 l = r4[q];
+    a = fmaf(-xr[q].x, l.x, a);
+    a = fmaf(-xr[q].y, l.y, a);
+    a = fmaf(-xr[q].z, l.z, a);
+    a = fmaf(-xr[q].w, l.w, a);
+    b = fmaf(xr[q].x, fabsf(l.x), b);
+    b = fmaf(xr[q].y, fabsf(l.y), b);
+    b = fmaf(xr[q].z, fabsf(l.z), b);
+    b = fmaf(xr[q].w, fabsf(l.w), b);
   }
   ce = a;
   ab = b;
@@ -205,7 +259,10 @@ __device__ __forceinline__ void exact_rank(const JoinParams &p, WarpTopK<KeyD, K
       key.id = ids[b + lane];
     }
     __syncwarp();
-    ex.insert(key, p.K, lane);
+    if (b == 0)
+      ex.first(key, lane);
+    else
+      ex.insert(key, p.K, lane);
   }
 }
 
@@ -405,7 +462,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
       __syncwarp();
       if (lane < nrow) {
         float ce, ab;
-        screen_row<NV4>(wstage + buf * wrows * ld + lane * ld, x32, ld, ce, ab);
+        screen_row<NV4>(wstage + buf * wrows * ld + lane * ld, x32, ld, p.nonpos, ce, ab);
         scores[k0 + lane] = ce;
         mn = fminf(mn, ce);
         mx = fmaxf(mx, ce);
@@ -569,6 +626,11 @@ __global__ void __launch_bounds__(128, 4) join_warp_kernel(JoinParams p, const i
     for (int i = lane; i < ld; i += 32) x32[i] = i < d ? (float)__ldg(p.points + (int64_t)x * d + i) : 0.f;
     for (int i = lane; i < d; i += 32) x64[i] = __ldg(p.points + (int64_t)x * d + i);
     __syncwarp();
+    float4 xreg[NV4 > 0 ? NV4 : 1];  // the anchor's fp32 row in registers
+    if constexpr (NV4 > 0) {
+#pragma unroll
+      for (int q = 0; q < NV4; ++q) xreg[q] = reinterpret_cast<const float4 *>(x32)[q];
+    }
 
     // ---- phase 1: dedup (no atomics)
     int U = 0;
@@ -610,16 +672,16 @@ __global__ void __launch_bounds__(128, 4) join_warp_kernel(JoinParams p, const i
             int claim = -1;
             if (pending) {
               const int4 v = reinterpret_cast<const int4 *>(table)[b];
-              if (v.x == y || v.y == y || v.z == y || v.w == y) {
+              const unsigned hit = (v.x == y) | (v.y == y) | (v.z == y) | (v.w == y);
+              const unsigned emp =
+                  (v.x == EMPTY) | ((v.y == EMPTY) << 1) | ((v.z == EMPTY) << 2) | ((v.w == EMPTY) << 3);
+              if (hit) {
                 pending = false;
+              } else if (emp) {
+                claim = (int)(b * 4) + __ffs(emp) - 1;
+                table[claim] = y;
               } else {
-                const int e = v.x == EMPTY ? 0 : v.y == EMPTY ? 1 : v.z == EMPTY ? 2 : v.w == EMPTY ? 3 : -1;
-                if (e >= 0) {
-                  claim = (int)(b * 4) + e;
-                  table[claim] = y;
-                } else {
-                  b = (b + 1) & bmask;
-                }
+                b = (b + 1) & bmask;
               }
             }
             __syncwarp();
@@ -659,7 +721,10 @@ __global__ void __launch_bounds__(128, 4) join_warp_kernel(JoinParams p, const i
       __syncwarp();
       if (lane < nrow) {
         float ce, ab;
-        screen_row<NV4>(stage + buf * rows * ld + lane * ld, x32, ld, ce, ab);
+        if constexpr (NV4 > 0)
+          screen_row_reg<NV4>(stage + buf * rows * ld + lane * ld, xreg, p.nonpos, ce, ab);
+        else
+          screen_row<NV4>(stage + buf * rows * ld + lane * ld, x32, ld, p.nonpos, ce, ab);
         scores[k0 + lane] = ce;
         am = fmaxf(am, ab);
         float v = ce;
@@ -678,8 +743,9 @@ __global__ void __launch_bounds__(128, 4) join_warp_kernel(JoinParams p, const i
     if (rows * Q >= K) {  // otherwise the kept subset may hold fewer than K values
       WarpTopK<KeyF, KPL> top;
       top.init();
+      top.first(KeyF{best[0]}, lane);
 #pragma unroll
-      for (int q = 0; q < Q; ++q) top.insert(KeyF{best[q]}, K, lane);
+      for (int q = 1; q < Q; ++q) top.insert(KeyF{best[q]}, K, lane);
       T = top.get(K - 1).v;  // >= the K-th smallest screened value (U >= K)
     }
     const float theta = T + 2.f * p.band * am + fabsf(T) * 1e-6f;
@@ -744,7 +810,7 @@ __global__ void classify_kernel(const int64_t *__restrict__ indptr, int64_t m, i
 // ---------------------------------------------------------------------------
 // host side: the size-class plan
 
-enum { KIND_WARP = 0, KIND_BLOCK128 = 1, KIND_BLOCK256 = 2, KIND_GLOBAL = 3 };
+enum { KIND_WARP = 0, KIND_BLOCK128 = 1, KIND_BLOCK256 = 2, KIND_GLOBAL = 3, KIND_BLOCK64 = 4 };
 
 struct Cls {
   int kind, logH, sw;
@@ -778,6 +844,9 @@ static int parse_plan(const char *spec, int kind[], int logH[]) {
     if (q[0] == 'w') {
       k = KIND_WARP;
       l = atoi(q + 1);
+    } else if (q[0] == 'b' && !strncmp(q + 1, "64:", 3)) {
+      k = KIND_BLOCK64;
+      l = atoi(q + 4);
     } else if (q[0] == 'b' && !strncmp(q + 1, "128:", 4)) {
       k = KIND_BLOCK128;
       l = atoi(q + 5);
@@ -940,6 +1009,8 @@ static int dispatch_class(const Plan &P, int i, const JoinParams &p, const int32
   switch (c.kind) {
     case KIND_WARP:
       return dispatch_warp(P, p, alist, acount, c.logH, c.sw, st);
+    case KIND_BLOCK64:
+      return dispatch_block<64, false>(P, p, alist, acount, c.logH, c.sw, nullptr, 0, 0, st);
     case KIND_BLOCK128:
       return dispatch_block<128, false>(P, p, alist, acount, c.logH, c.sw, nullptr, 0, 0, st);
     case KIND_BLOCK256:
@@ -966,7 +1037,7 @@ int knnd_local_join(const double *points, const float *log32, const double *log6
                     int32_t d, int32_t ld32, const int32_t *friends, int32_t k, const int64_t *indptr,
                     const int32_t *indices, int64_t row_lo, int64_t row_hi, int32_t max_indeg, int32_t *out_ids,
                     double *out_kl, int32_t *out_ucount, unsigned long long *tally, void *ws, size_t ws_bytes,
-                    void *stream) {
+                    uint32_t flags, void *stream) {
   KNND_CHECK_ARG(points && log32 && log64 && xlogx && friends && indptr && indices && out_ids && tally,
                  "knnd_local_join: null pointer");
   KNND_CHECK_ARG(n >= 2 && d >= 1, "knnd_local_join: bad shape n=%lld d=%d", (long long)n, d);
@@ -1013,6 +1084,7 @@ int knnd_local_join(const double *points, const float *log32, const double *log6
   p.K = k;
   // rigorous bound on |fp32 screen - fp64| relative to sum |x*log y| (+ margin)
   p.band = (float)((ld32 + 8) * 0x1p-24);
+  p.nonpos = (flags & KNND_JOIN_NONPOS_LOG) ? 1 : 0;
 
   KNND_CUDA(cudaMemsetAsync(counts, 0, 64, st));
   {

@@ -86,7 +86,10 @@ class CudaOps:
         return Csr(indptr, indices, lo, hi)
 
     def join(self, tabs, table: torch.Tensor, n: int, k: int, csr: Csr, max_indeg: int, out_rows: torch.Tensor,
-             tally: torch.Tensor, out_kl: torch.Tensor | None = None, out_ucount: torch.Tensor | None = None) -> None:
+             tally: torch.Tensor, out_kl: torch.Tensor | None = None, out_ucount: torch.Tensor | None = None,
+             flags: int | None = None) -> None:
+        if flags is None:
+            flags = _lib.JOIN_NONPOS_LOG if tabs.max_coord <= 1.0 else 0
         nbytes = _lib.load().knnd_local_join_workspace_bytes(n, tabs.d, k, csr.lo, csr.hi, max_indeg)
         ws = self._workspace("join", nbytes)
         _lib.call("knnd_local_join", tabs.points.data_ptr(), tabs.log32.data_ptr(), tabs.log64.data_ptr(),
@@ -94,7 +97,7 @@ class CudaOps:
                   csr.indices.data_ptr(), csr.lo, csr.hi, max_indeg, out_rows.data_ptr(),
                   out_kl.data_ptr() if out_kl is not None else None,
                   out_ucount.data_ptr() if out_ucount is not None else None, tally.data_ptr(), ws.data_ptr(),
-                  ws.numel(), self._stream())
+                  ws.numel(), flags, self._stream())
 
     def fcc(self, table: torch.Tensor, n: int, k: int, samples: torch.Tensor, out_count: torch.Tensor) -> None:
         s = samples.shape[1]

@@ -150,6 +150,46 @@ def test_ucount_and_kl_values_vs_oracle(cuda, small_meta, small_tables):
     assert tally.cpu().tolist()[:3] == [o_comp, o_changed, 0]
 
 
+def test_join_flags_do_not_change_results(cuda, small_meta, small_tables):
+    """KNND_JOIN_NONPOS_LOG only skips an accumulator that equals the other one."""
+    name = "n1000_d20_k20_s1"
+    meta = small_meta[name]
+    pts = _points(meta)
+    n, k = meta["n"], meta["k"]
+    rs = b2.KlRankingSystem(pts, validate=False)
+    tabs = rs.device_tables()
+    st = b2.KnnState(small_tables[f"{name}/init"])
+    outs = []
+    for flags in (0, 1):
+        out = torch.empty((n, k), dtype=torch.int32, device=cuda)
+        kl = torch.empty((n, k), dtype=torch.float64, device=cuda)
+        tally = torch.zeros(4, dtype=torch.int64, device=cuda)
+        st._engine.ops.join(tabs, st._table, n, k, st._csr, st._max_indeg, out, tally, kl, None, flags=flags)
+        outs.append((out.cpu().numpy(), kl.cpu().numpy(), tally.cpu().tolist()))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])
+    assert outs[0][2] == outs[1][2]
+
+
+def test_non_simplex_points_use_general_bound(cuda):
+    """Coordinates > 1 (positive logs): the screen's bound must use sum |x log y|."""
+    rng = np.random.default_rng(4)
+    pts = rng.uniform(0.2, 3.0, size=(3000, 20))  # not on the simplex; KL-style scores still defined
+    rs = b2.KlRankingSystem(pts, validate=False)
+    assert rs.device_tables().max_coord > 1.0
+    table = native.sort_rows(native.Tables(pts), b2.random_kout_draws(3000, 10, rng))
+    st = b2.KnnState(table)
+    out = torch.empty((3000, 10), dtype=torch.int32, device=cuda)
+    tally = torch.zeros(4, dtype=torch.int64, device=cuda)
+    st._engine.ops.join(rs.device_tables(), st._table, 3000, 10, st._csr, st._max_indeg, out, tally)
+    o_rows, _, _, o_comp, o_changed = native.local_join(native.Tables(pts), table)
+    got = out.cpu().numpy()
+    if not np.array_equal(got, o_rows):
+        diff = tie_aware_diff(native.Tables(pts), o_rows, got)
+        assert not diff["violations"], diff
+    assert tally.cpu().tolist()[:2] == [o_comp, o_changed]
+
+
 def _hub_table(n, k, hubs, rng):
     """Random K-out table where `hubs[i]` receives about counts[i] extra arcs."""
     t = b2.random_kout_draws(n, k, rng)

@@ -3,7 +3,8 @@ import csv, subprocess, sys
 from collections import defaultdict
 
 rep = sys.argv[1]
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
+extra = sys.argv[3:]  # e.g. --launch-skip 1 --launch-count 1
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass", *extra],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 agg = defaultdict(lambda: [0, 0, ""])
