@@ -132,6 +132,26 @@ int knnd_sort_rows(const double *points, const double *log64, const double *xlog
                    int64_t n, int32_t d, int32_t k, int64_t row_lo, int64_t row_hi,
                    const int32_t *draws, int32_t *out_ids, double *out_kl, void *stream);
 
+/*
+ * The initial random K-out draws on the device, bit-identical to numpy —
+ * init_random_kout's first draw (descent.py:194-197):
+ *   draws = Generator(PCG64).integers(0, n - 1, size=(n, k), dtype=int64)
+ *   draws += draws >= row
+ * (state_hi, state_lo, inc_hi, inc_lo, has_uint32, uinteger) is the PCG64
+ * state numpy reports in `bit_generator.state` before the call.
+ *   out       int32 (n, k): the draws
+ *   consumed  (device uint64) number of 32-bit values taken from the stream
+ *             (counting a buffered half), so the caller can advance its numpy
+ *             generator and continue the rejection loop (descent.py:198-205)
+ *   bad/nbad  (device) rows containing a repeated id, unordered, and their count
+ * Requires n - 1 <= 2^32 - 1 and n*k < 2^31.
+ */
+size_t knnd_random_kout_workspace_bytes(int64_t n, int32_t k);
+int knnd_random_kout(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                     int32_t has_uint32, uint32_t uinteger, int64_t n, int32_t k, int32_t *out,
+                     uint64_t *consumed, int32_t *bad, int32_t *nbad, void *ws, size_t ws_bytes,
+                     void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,18 +66,23 @@ __host__ __device__ inline size_t al16(size_t v) { return (v + 15) & ~(size_t)15
 
 __device__ __forceinline__ unsigned hash_slot(int y, unsigned shift) { return ((unsigned)y * 0x9E3779B1u) >> shift; }
 
-// block-wide insert (several warps share the table): CAS
+// block-wide insert (several warps share the table): 4-slot buckets, one int4
+// read finds a duplicate without atomics; new ids CAS the first empty slot
 __device__ __forceinline__ bool hash_insert_cas(int32_t *table, int y, unsigned shift, unsigned mask) {
-  unsigned h = hash_slot(y, shift);
+  const unsigned bmask = mask >> 2;
+  unsigned b = hash_slot(y, shift + 2);
   while (true) {
-    const int cur = *reinterpret_cast<volatile int32_t *>(table + h);
-    if (cur == y) return false;
-    if (cur == EMPTY) {
-      const int prev = atomicCAS(table + h, EMPTY, y);
+    asm volatile("" ::: "memory");  // re-read the bucket every pass (other warps insert concurrently)
+    const int4 v = reinterpret_cast<const int4 *>(table)[b];
+    if ((v.x == y) | (v.y == y) | (v.z == y) | (v.w == y)) return false;
+    const unsigned emp = (v.x == EMPTY) | ((v.y == EMPTY) << 1) | ((v.z == EMPTY) << 2) | ((v.w == EMPTY) << 3);
+    if (emp) {
+      const int prev = atomicCAS(table + b * 4 + (__ffs(emp) - 1), EMPTY, y);
       if (prev == EMPTY) return true;
       if (prev == y) return false;
+      continue;  // lost the slot to another id: re-read the bucket
     }
-    h = (h + 1) & mask;
+    b = (b + 1) & bmask;
   }
 }
 
@@ -117,6 +122,25 @@ __device__ __forceinline__ void stage_rows_f32(float *stage, const float *__rest
     for (int r = 0; r < nrow; ++r)
       for (int part = lane; part < nv4; part += 32)
         cp_async16(stage + r * ld + part * 4, log32 + (int64_t)ids[r] * ld + part * 4);
+  }
+}
+
+// same, with the row ids held in registers: lane r holds ids of row r of the
+// batch (nrow <= 32), rows are fetched with a shuffle
+template <int NV4>
+__device__ __forceinline__ void stage_rows_f32_reg(float *stage, const float *__restrict__ log32, int idreg,
+                                                   int nrow, int lane) {
+  constexpr int ld = NV4 * 4;
+  constexpr int rpi = 32 / NV4;
+  const int r0 = lane / NV4, part = lane - r0 * NV4;
+  unsigned dst = smem_u32(stage) + (unsigned)(r0 * ld + part * 4) * 4u;
+  const float *src = log32 + part * 4;
+  const int iters = (nrow + rpi - 1) / rpi;
+  for (int t = 0; t < iters; ++t, dst += rpi * ld * 4u) {
+    const int r = r0 + t * rpi;
+    const int y = __shfl_sync(FULL, idreg, r & 31);
+    if (r0 < rpi && r < nrow)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src + (int64_t)y * ld) : "memory");
   }
 }
 
@@ -250,7 +274,22 @@ __device__ __forceinline__ void exact_rank(const JoinParams &p, WarpTopK<KeyD, K
   ex.init();
   for (int b = 0; b < nR; b += rcap) {
     const int nrow = min(rcap, nR - b);
-    stage_rows_f64(stage64, sd, p.log64, ids + b, nrow, d, lane);
+    {  // row ids of this batch in registers, fetched once per lane
+      const int idreg = lane < nrow ? ids[b + lane] : 0;
+      const int nchunk = nrow * d;
+      const int rq = 32 / d, rr = 32 - rq * d;
+      int r = lane / d, j = lane - (lane / d) * d;
+      for (int c0 = 0; c0 < nchunk; c0 += 32) {
+        const int y = __shfl_sync(FULL, idreg, r & 31);
+        if (c0 + lane < nchunk) cp_async8(stage64 + r * sd + j, p.log64 + (int64_t)y * d + j);
+        r += rq;
+        j += rr;
+        if (j >= d) {
+          j -= d;
+          ++r;
+        }
+      }
+    }
     cp_async_wait_all();
     __syncwarp();
     KeyD key = KeyD::inf();
@@ -581,21 +620,23 @@ __host__ __device__ inline WarpSlab warp_slab(int d, int ld, int H, int SW) {
   return L;
 }
 
-template <int NV4, int KPL>
-__global__ void __launch_bounds__(128, 4) join_warp_kernel(JoinParams p, const int32_t *__restrict__ alist,
-                                                        const int32_t *__restrict__ acount, int logH, int SW) {
+template <int NV4, int KPL, bool GLIST>
+__global__ void __launch_bounds__(128, GLIST ? 6 : 4)
+    join_warp_kernel(JoinParams p, const int32_t *__restrict__ alist, const int32_t *__restrict__ acount, int logH,
+                     int SW, int32_t *__restrict__ glists) {
   constexpr int Q = 2 * KPL;  // per-lane kept screened values
   extern __shared__ __align__(16) unsigned char sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int H = 1 << logH;
   const unsigned shift = 32u - (unsigned)logH, bmask = ((unsigned)H >> 2) - 1u;
   const WarpSlab L = warp_slab(p.d, p.ld, H, SW);
-  unsigned char *base = sm + (size_t)warp * L.total;
+  unsigned char *base = sm + (size_t)warp * (GLIST ? L.list : L.total);  // GLIST: no list in smem
   float *x32 = reinterpret_cast<float *>(base + L.x32);
   double *x64 = reinterpret_cast<double *>(base + L.x64);
   int32_t *S = reinterpret_cast<int32_t *>(base + L.S);
   int32_t *table = reinterpret_cast<int32_t *>(base + L.table);
-  int32_t *list = reinterpret_cast<int32_t *>(base + L.list);
+  int32_t *list = GLIST ? glists + (size_t)(blockIdx.x * (blockDim.x >> 5) + warp) * (H >> 1)
+                        : reinterpret_cast<int32_t *>(base + L.list);
   float *scores = reinterpret_cast<float *>(table);            // phase 2-3: [0, U)
   float *stage = reinterpret_cast<float *>(table + (H >> 1));  // phase 2: upper half
   double *stage64 = reinterpret_cast<double *>(table);         // phase 4: whole table
@@ -704,16 +745,27 @@ __global__ void __launch_bounds__(128, 4) join_warp_kernel(JoinParams p, const i
 #pragma unroll
     for (int q = 0; q < Q; ++q) best[q] = __int_as_float(0x7f800000);
     float am = 0.f;
+    // ids of batch b+1 are in a register while batch b computes; batch b+2's are being loaded
+    int id_next = (lane < min(rows, U)) ? list[lane] : 0;
+    int id_after = (rows + lane < U && lane < rows) ? list[rows + lane] : 0;
     if (U > 0) {
-      stage_rows_f32<NV4>(stage, p.log32, list, min(rows, U), ld, lane);
+      if constexpr (NV4 > 0)
+        stage_rows_f32_reg<NV4>(stage, p.log32, id_next, min(rows, U), lane);
+      else
+        stage_rows_f32<NV4>(stage, p.log32, list, min(rows, U), ld, lane);
       cp_async_commit();
     }
     for (int k0 = 0, buf = 0; k0 < U; k0 += rows, buf ^= 1) {
       const int nrow = min(rows, U - k0);
       if (k0 + rows < U) {  // prefetch the next batch into the other buffer
-        stage_rows_f32<NV4>(stage + (buf ^ 1) * rows * ld, p.log32, list + k0 + rows, min(rows, U - k0 - rows), ld,
-                            lane);
+        const int n1 = min(rows, U - k0 - rows);
+        if constexpr (NV4 > 0)
+          stage_rows_f32_reg<NV4>(stage + (buf ^ 1) * rows * ld, p.log32, id_after, n1, lane);
+        else
+          stage_rows_f32<NV4>(stage + (buf ^ 1) * rows * ld, p.log32, list + k0 + rows, n1, ld, lane);
         cp_async_commit();
+        const int k2 = k0 + 2 * rows;
+        id_after = (lane < rows && k2 + lane < U) ? list[k2 + lane] : 0;
         cp_async_wait_1();
       } else {
         cp_async_wait_0();
@@ -810,7 +862,7 @@ __global__ void classify_kernel(const int64_t *__restrict__ indptr, int64_t m, i
 // ---------------------------------------------------------------------------
 // host side: the size-class plan
 
-enum { KIND_WARP = 0, KIND_BLOCK128 = 1, KIND_BLOCK256 = 2, KIND_GLOBAL = 3, KIND_BLOCK64 = 4 };
+enum { KIND_WARP = 0, KIND_BLOCK128 = 1, KIND_BLOCK256 = 2, KIND_GLOBAL = 3, KIND_BLOCK64 = 4, KIND_WARPG = 5 };
 
 struct Cls {
   int kind, logH, sw;
@@ -823,7 +875,8 @@ struct Plan {
   Cls c[MAXCLS];
   int nslab;
   int64_t slab_ints;
-  size_t lists_off, counts_off, slab_off, total;
+  int64_t glist_ints;  // per-warp global unique lists (KIND_WARPG)
+  size_t lists_off, counts_off, slab_off, glist_off, total;
 };
 
 constexpr int WARP_BLOCK = 128, GL = 512;
@@ -843,6 +896,9 @@ static int parse_plan(const char *spec, int kind[], int logH[]) {
     int k, l = 0;
     if (q[0] == 'w') {
       k = KIND_WARP;
+      l = atoi(q + 1);
+    } else if (q[0] == 'g') {
+      k = KIND_WARPG;
       l = atoi(q + 1);
     } else if (q[0] == 'b' && !strncmp(q + 1, "64:", 3)) {
       k = KIND_BLOCK64;
@@ -915,6 +971,12 @@ static Plan make_plan(int64_t m, int d, int K, int max_indeg) {
   P.ncls = n + 1;
   P.nslab = g.need ? 2 * num_sms() : 0;
   P.slab_ints = g.need ? (int64_t)align_up((size_t)g.sw + ((size_t)3 << g.logH) / 2, 64) : 0;
+  P.glist_ints = 0;
+  for (int i = 0; i < n; ++i)
+    if (P.c[i].kind == KIND_WARPG && P.c[i].need) {
+      const int64_t per = (int64_t)num_sms() * 64 * (((int64_t)1 << P.c[i].logH) / 2);  // <= 64 warps per SM
+      if (per > P.glist_ints) P.glist_ints = per;
+    }
   size_t o = 0;
   P.lists_off = o;
   o = align_up(o + (size_t)P.ncls * m * 4, 256);
@@ -922,6 +984,8 @@ static Plan make_plan(int64_t m, int d, int K, int max_indeg) {
   o = align_up(o + 64, 256);
   P.slab_off = o;
   o = align_up(o + (size_t)P.nslab * P.slab_ints * 4, 256);
+  P.glist_off = o;
+  o = align_up(o + (size_t)P.glist_ints * 4, 256);
   P.total = o;
   return P;
 }
@@ -950,11 +1014,12 @@ static int launch_join(const JoinParams &p, const int32_t *alist, const int32_t 
   return KNND_OK;
 }
 
-template <int NV4, int KPL>
+template <int NV4, int KPL, bool GLIST>
 static int launch_warp(const JoinParams &p, const int32_t *alist, const int32_t *acount, int logH, int SW,
-                       cudaStream_t st) {
-  auto kern = join_warp_kernel<NV4, KPL>;
-  const WarpSlab L = warp_slab(p.d, p.ld, 1 << logH, SW);
+                       int32_t *glists, cudaStream_t st) {
+  auto kern = join_warp_kernel<NV4, KPL, GLIST>;
+  WarpSlab L = warp_slab(p.d, p.ld, 1 << logH, SW);
+  if (GLIST) L.total = L.list;  // the unique list lives in the global slab
   const size_t smem = L.total * (WARP_BLOCK / 32);
   if (smem > 227 * 1024) {
     set_error("local join: warp slabs %zu B exceed 227 KB (d=%d, H=%d)", smem, p.d, 1 << logH);
@@ -967,7 +1032,8 @@ static int launch_warp(const JoinParams &p, const int32_t *alist, const int32_t 
     set_error("local join: warp kernel cannot be resident (smem=%zu)", smem);
     return KNND_EUNSUPPORTED;
   }
-  kern<<<per_sm * num_sms(), WARP_BLOCK, smem, st>>>(p, alist, acount, logH, SW);
+  if (GLIST && per_sm > 16) per_sm = 16;  // the workspace holds 64 warp lists per SM
+  kern<<<per_sm * num_sms(), WARP_BLOCK, smem, st>>>(p, alist, acount, logH, SW, glists);
   KNND_LAUNCHED(1);
   return KNND_OK;
 }
@@ -992,23 +1058,26 @@ static int dispatch_block(const Plan &P, const JoinParams &p, const int32_t *ali
 #undef KNND_CALL
 }
 
+template <bool GLIST>
 static int dispatch_warp(const Plan &P, const JoinParams &p, const int32_t *alist, const int32_t *acount, int logH,
-                         int SW, cudaStream_t st) {
-#define KNND_CALL(NV)                                                      \
-  return P.kpl == 1 ? launch_warp<NV, 1>(p, alist, acount, logH, SW, st) \
-                    : launch_warp<NV, 2>(p, alist, acount, logH, SW, st)
+                         int SW, int32_t *glists, cudaStream_t st) {
+#define KNND_CALL(NV)                                                                     \
+  return P.kpl == 1 ? launch_warp<NV, 1, GLIST>(p, alist, acount, logH, SW, glists, st) \
+                    : launch_warp<NV, 2, GLIST>(p, alist, acount, logH, SW, glists, st)
   KNND_NV_SWITCH(KNND_CALL)
 #undef KNND_CALL
 }
 
 static int dispatch_class(const Plan &P, int i, const JoinParams &p, const int32_t *lists, const int32_t *counts,
-                          int64_t m, int32_t *slabs, cudaStream_t st) {
+                          int64_t m, int32_t *slabs, int32_t *glists, cudaStream_t st) {
   const Cls &c = P.c[i];
   const int32_t *alist = lists + (int64_t)i * m;
   const int32_t *acount = counts + i;
   switch (c.kind) {
     case KIND_WARP:
-      return dispatch_warp(P, p, alist, acount, c.logH, c.sw, st);
+      return dispatch_warp<false>(P, p, alist, acount, c.logH, c.sw, nullptr, st);
+    case KIND_WARPG:
+      return dispatch_warp<true>(P, p, alist, acount, c.logH, c.sw, glists, st);
     case KIND_BLOCK64:
       return dispatch_block<64, false>(P, p, alist, acount, c.logH, c.sw, nullptr, 0, 0, st);
     case KIND_BLOCK128:
@@ -1065,6 +1134,7 @@ int knnd_local_join(const double *points, const float *log32, const double *log6
   int32_t *lists = reinterpret_cast<int32_t *>(w + P.lists_off);
   int32_t *counts = reinterpret_cast<int32_t *>(w + P.counts_off);
   int32_t *slabs = reinterpret_cast<int32_t *>(w + P.slab_off);
+  int32_t *glists = reinterpret_cast<int32_t *>(w + P.glist_off);
 
   JoinParams p;
   p.points = points;
@@ -1099,7 +1169,7 @@ int knnd_local_join(const double *points, const float *log32, const double *log6
   // biggest tables first: the few long hub anchors start early
   for (int i = P.ncls - 1; i >= 0; --i) {
     if (!P.c[i].need) continue;
-    const int rc = dispatch_class(P, i, p, lists, counts, m, slabs, st);
+    const int rc = dispatch_class(P, i, p, lists, counts, m, slabs, glists, st);
     if (rc) return rc;
   }
   return KNND_OK;

@@ -232,6 +232,69 @@ def random_kout_draws(n: int, k: int, rng: np.random.Generator) -> np.ndarray:
     return draws
 
 
+_M64 = (1 << 64) - 1
+_M128 = (1 << 128) - 1
+_PCG_MULT = 0x2360ED051FC65DA44385DF649FCCF645  # PCG64 (XSL-RR 128/64) multiplier
+
+
+def _pcg_output(s: int) -> int:
+    x = (s >> 64) ^ (s & _M64)
+    rot = s >> 122
+    return ((x >> rot) | (x << ((64 - rot) & 63))) & _M64
+
+
+def _pcg_advance(s: int, inc: int, steps: int) -> int:
+    """The PCG64 state after `steps` 64-bit outputs (LCG jump-ahead)."""
+    a, c = _PCG_MULT, inc
+    acc_a, acc_c = 1, 0
+    while steps:
+        if steps & 1:
+            acc_a, acc_c = (a * acc_a) & _M128, (a * acc_c + c) & _M128
+        c = (a * c + c) & _M128
+        a = (a * a) & _M128
+        steps >>= 1
+    return (acc_a * s + acc_c) & _M128
+
+
+def device_random_kout(eng: Engine, n: int, k: int, rng: np.random.Generator, table: torch.Tensor) -> bool:
+    """descent.py:194-205 with the first (n, K) draw made on the device by a
+    bit-exact replica of numpy's PCG64 + Lemire stream (knnd_random_kout); the
+    numpy generator is then advanced past the values the device consumed and
+    the rejection redraws of rows with duplicates run on the host, exactly as
+    the reference does them.  Returns False (nothing done) when the generator is
+    not PCG64 or the ops have no device path."""
+    st = rng.bit_generator.state
+    if st.get("bit_generator") != "PCG64" or not hasattr(eng.ops, "random_kout") or n - 1 > 0xFFFFFFFF:
+        return False
+    s0, inc = int(st["state"]["state"]), int(st["state"]["inc"])
+    has, uint = int(st["has_uint32"]), int(st["uinteger"])
+    meta = torch.zeros(2, dtype=torch.int64, device=eng.device)
+    bad_dev = torch.empty(n, dtype=torch.int32, device=eng.device)
+    eng.ops.random_kout((s0, inc, has, uint), n, k, table, meta, bad_dev)
+    consumed, nbad = (int(v) for v in meta.cpu().tolist())  # nbad: an int32 in the low half of meta[1]
+    fresh = consumed - has
+    if has and fresh < 0:
+        fresh = 0
+    s1 = _pcg_advance(s0, inc, (fresh + 1) // 2)
+    left = fresh % 2 == 1
+    rng.bit_generator.state = {"bit_generator": "PCG64", "state": {"state": s1, "inc": inc},
+                               "has_uint32": 1 if left else 0, "uinteger": (_pcg_output(s1) >> 32) if left else 0}
+    if nbad:
+        bad = np.sort(bad_dev[:nbad].cpu().numpy().astype(np.int64))
+        rows = bad.copy()
+        fixed = {}
+        while bad.size:  # descent.py:198-205, restricted to the rows that can still change
+            redraw = rng.integers(0, n - 1, size=(bad.size, k), dtype=np.int64)
+            redraw += redraw >= bad[:, None]
+            for r, row in zip(bad, redraw):
+                fixed[int(r)] = row
+            srt = np.sort(redraw, axis=1)
+            bad = bad[(srt[:, 1:] == srt[:, :-1]).any(axis=1)]
+        vals = torch.from_numpy(np.stack([fixed[int(r)] for r in rows]).astype(np.int32)).to(eng.device)
+        table[torch.from_numpy(rows).to(eng.device)] = vals
+    return True
+
+
 def fcc_samples(n: int, k: int, count: int, rng: np.random.Generator) -> np.ndarray:
     """descent.py:330-333 — (3, count) int32: anchors, slot i, slot j != i."""
     xs = rng.integers(0, n, size=count)
@@ -259,9 +322,13 @@ def init_random_kout(dataset: Dataset, rs, cfg: DescentConfig, rng: np.random.Ge
     if n <= k:
         raise ConfigError(f"need n > k, got n={n}, k={k}")
     tabs = device_tables_for(rs, device)
-    draws = random_kout_draws(n, k, rng)
     eng = Engine(n, k, tabs.device)
-    table = eng.init_rows(tabs, draws)
+    table = eng.alloc_table()
+    if not (n - 1 > 2 * k * k and device_random_kout(eng, n, k, rng, table)):
+        eng.upload_rows(random_kout_draws(n, k, rng), table)
+    s = eng.shard
+    eng.ops.sort_rows(tabs, eng.own_rows(table), k, s.lo, s.hi)
+    eng.exchange(table)
     csr, mx = eng.build_csr(table)
     return KnnState._from_device(eng, table, csr, mx, 0, ())
 
@@ -359,10 +426,11 @@ def _run_rounds(dataset: Dataset, rs, cfg: DescentConfig, max_rounds: int, stop_
     if n <= k:
         raise ConfigError(f"need n > k, got n={n}, k={k}")
     tabs = device_tables_for(rs)
-    draws = random_kout_draws(n, k, derive_rng(cfg.seed, STREAM_INIT))
     eng = Engine(n, k, tabs.device)
     table = eng.alloc_table()
-    eng.upload_rows(draws, table)
+    rng = derive_rng(cfg.seed, STREAM_INIT)
+    if not (n - 1 > 2 * k * k and device_random_kout(eng, n, k, rng, table)):
+        eng.upload_rows(random_kout_draws(n, k, rng), table)
     smp_dev = _to_device(draw_fcc_schedule(n, k, cfg, max_rounds), tabs.device)
     state, history = descend_resident(eng, tabs, table, smp_dev, cfg.fcc_sample_count, max_rounds,
                                       stop_on_fixed_point)

@@ -99,6 +99,18 @@ class CudaOps:
                   out_ucount.data_ptr() if out_ucount is not None else None, tally.data_ptr(), ws.data_ptr(),
                   ws.numel(), flags, self._stream())
 
+    def random_kout(self, state: tuple, n: int, k: int, table: torch.Tensor, out_meta: torch.Tensor,
+                    bad: torch.Tensor) -> None:
+        """numpy's PCG64 integers(0, n-1, (n, k)) + row shift on the device (knnd_random_kout).
+        out_meta (int64, 2): [0] u32 values consumed, [1] number of rows with duplicates."""
+        s, inc, has, uint = state
+        m64 = (1 << 64) - 1
+        nbytes = _lib.load().knnd_random_kout_workspace_bytes(n, k)
+        ws = self._workspace("rng", nbytes)
+        _lib.call("knnd_random_kout", s >> 64, s & m64, inc >> 64, inc & m64, has, uint, n, k, table.data_ptr(),
+                  out_meta.data_ptr(), bad.data_ptr(), out_meta[1:].view(torch.int32).data_ptr(), ws.data_ptr(),
+                  ws.numel(), self._stream())
+
     def fcc(self, table: torch.Tensor, n: int, k: int, samples: torch.Tensor, out_count: torch.Tensor) -> None:
         s = samples.shape[1]
         _lib.call("knnd_fcc", table.data_ptr(), n, k, samples[0].data_ptr(), samples[1].data_ptr(),

@@ -54,6 +54,30 @@ def test_batch_scores_pins_and_batch_independence(cuda, known):
 
 
 # ---------------------------------------------------------------------------
+# device replica of numpy's PCG64 draws (init_random_kout, descent.py:194-205)
+
+
+@pytest.mark.parametrize("n,k,seed,pre", [(1000, 20, 0, 0), (300, 7, 3, 0), (1_000_000, 20, 0, 0),
+                                          (100_000, 20, 5, 1), (3_000_001, 7, 2, 3), (50_000, 64, 9, 0)])
+def test_device_random_kout_matches_numpy(cuda, n, k, seed, pre):
+    """Same table as the host draws (incl. rows with duplicates, redrawn on the
+    host), and the generator continues exactly where numpy's would."""
+    from paper_2202_00517_b200.descent import device_random_kout
+
+    rng_host = b2.derive_rng(seed, 2)
+    rng_dev = b2.derive_rng(seed, 2)
+    for _ in range(pre):  # leave a buffered 32-bit half (has_uint32) in some cases
+        assert rng_host.integers(0, 1000) == rng_dev.integers(0, 1000)
+    expect = b2.random_kout_draws(n, k, rng_host)
+    eng = Engine(n, k, cuda)
+    table = eng.alloc_table()
+    assert device_random_kout(eng, n, k, rng_dev, table)
+    assert np.array_equal(table[:n].cpu().numpy(), expect.astype(np.int32))
+    assert rng_dev.bit_generator.state == rng_host.bit_generator.state
+    assert np.array_equal(rng_dev.integers(0, 1 << 40, 16), rng_host.integers(0, 1 << 40, 16))
+
+
+# ---------------------------------------------------------------------------
 # K1 co-friend CSR
 
 
