@@ -161,8 +161,14 @@ class KnnState:
 
     @property
     def friends(self) -> np.ndarray:
-        if self._host is None:
-            host = self._table[: self.n].cpu().numpy().astype(np.int64)
+        if self._host is None:  # widen on the device, one D2H copy into (cached) pinned memory
+            dev64 = self._table[: self.n].to(torch.int64)
+            if dev64.is_cuda:
+                pinned = torch.empty(dev64.shape, dtype=torch.int64, pin_memory=True)
+                pinned.copy_(dev64)
+                host = pinned.numpy()
+            else:
+                host = dev64.numpy().copy()
             host.flags.writeable = False
             self._host = host
         return self._host

@@ -70,7 +70,7 @@ def _dev(device) -> torch.device:
 class DeviceTables:
     """The per-device copy of one KlRankingSystem's tables."""
 
-    def __init__(self, points: np.ndarray, device: torch.device, pinned: bool = True):
+    def __init__(self, points: np.ndarray, device: torch.device, pinned: bool = False):
         self.device = device
         self.n, self.d = points.shape
         self.ld = (self.d + 3) // 4 * 4
