@@ -194,14 +194,17 @@ __device__ __forceinline__ void screen_row_reg(const float *row, const float4 (&
   const float4 *r4 = reinterpret_cast<const float4 *>(row);
   float a = 0.f, b = 0.f;
   if (nonpos) {
+    // four independent chains (the error bound holds for any order of same-sign terms)
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
     for (int q = 0; q < NV4; ++q) {
       const float4 l = r4[q];
-      a = fmaf(-xr[q].x, l.x, a);
-      a = fmaf(-xr[q].y, l.y, a);
-      a = fmaf(-xr[q].z, l.z, a);
-      a = fmaf(-xr[q].w, l.w, a);
+      a0 = fmaf(-xr[q].x, l.x, a0);
+      a1 = fmaf(-xr[q].y, l.y, a1);
+      a2 = fmaf(-xr[q].z, l.z, a2);
+      a3 = fmaf(-xr[q].w, l.w, a3);
     }
+    a = (a0 + a1) + (a2 + a3);
     ce = a;
     ab = a;
     return;
