@@ -79,6 +79,20 @@ struct KeyD {
   }
 };
 
+// screened value with its id (the order used to certify a row without fp64)
+struct KeyFI {
+  float v;
+  int id;
+  __device__ __forceinline__ static KeyFI inf() { return {__int_as_float(0x7f800000), 0x7fffffff}; }
+  __device__ __forceinline__ bool lt(const KeyFI &o) const { return v < o.v || (v == o.v && id < o.id); }
+  __device__ __forceinline__ KeyFI shfl(int src) const {
+    return {__shfl_sync(FULL, v, src), __shfl_sync(FULL, id, src)};
+  }
+  __device__ __forceinline__ KeyFI shfl_xor(int m) const {
+    return {__shfl_xor_sync(FULL, v, m), __shfl_xor_sync(FULL, id, m)};
+  }
+};
+
 template <class Key>
 __device__ __forceinline__ Key kmin(const Key &a, const Key &b) { return b.lt(a) ? b : a; }
 template <class Key>

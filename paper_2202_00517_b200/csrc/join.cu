@@ -308,11 +308,37 @@ __device__ __forceinline__ void exact_rank(const JoinParams &p, WarpTopK<KeyD, K
   }
 }
 
+// Phase 4 without fp64 when the screen already decides the row: sort R (<= 32)
+// by (screened value, id); if each of the first K screened values is below the
+// next one by more than the error band 2c*am (+ margin), the exact order of the
+// top K+1 — hence the row — is the screened order (exact ties are impossible
+// at that distance).  Returns false (nothing written) when a gap is too small.
+__device__ __forceinline__ bool certify_row(const JoinParams &p, const int32_t *ids, const float *vals, int nR,
+                                            float am, int x, int64_t xr, int lane, bool &diff) {
+  const int K = p.K;
+  KeyFI key = KeyFI::inf();
+  if (lane < nR) key = {vals[lane], ids[lane]};
+  key = warp_sort32(key, lane);
+  const float nextv = __shfl_down_sync(FULL, key.v, 1);
+  const float band = 2.f * p.band * am;
+  const float gap_need = band + fabsf(key.v) * 2e-6f + 1e-30f;
+  const bool need_check = lane < K && lane + 1 < nR;  // nR == K: the set is R itself
+  const bool ok = !need_check || (nextv - key.v > gap_need);
+  if (!__all_sync(FULL, ok)) return false;
+  bool d = false;
+  if (lane < K) {
+    p.out_ids[xr * K + lane] = key.id;
+    d = key.id != __ldg(p.F + (int64_t)x * K + lane);
+  }
+  diff = __any_sync(FULL, d);
+  return true;
+}
+
 // ---------------------------------------------------------------------------
 // block-per-anchor kernel (classes B and L)
 
 struct SmemLayout {
-  size_t x32, x64, red, hist, stage, S, table, list, total;
+  size_t x32, x64, red, hist, rval, stage, S, table, list, total;
 };
 
 constexpr int NBIN = 256;        // histogram-select buckets per pass
@@ -329,6 +355,8 @@ __host__ __device__ inline SmemLayout smem_layout(int G, bool gtab, int d, int l
   o = al16(o + (size_t)(G / 32) * 4 * 4);
   L.hist = o;
   o = al16(o + (size_t)2 * NBIN * 4);
+  L.rval = o;  // screened values of the first 32 members of R
+  o = al16(o + 32 * 4);
   if (!gtab) {
     L.stage = 0;  // staging uses the (dead) table
     L.S = o;
@@ -398,6 +426,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
   float *red = reinterpret_cast<float *>(sm + L.red);
   int *hist = reinterpret_cast<int *>(sm + L.hist);
   int *hist2 = hist + NBIN;
+  float *rval = reinterpret_cast<float *>(sm + L.rval);
   int32_t *S, *table, *list;
   float *wstage;  // this warp's fp32 staging rows
   double *stage64;
@@ -563,8 +592,20 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
       const int iters = (U + G - 1) / G;
       for (int it = 0; it < iters; ++it) {
         const int k = it * G + tid;
-        const bool take = k < U && scores[k] <= theta;
-        warp_append(take, take ? list[k] : 0, &hdr[1], R, lane);
+        const float v = k < U ? scores[k] : 0.f;
+        const bool take = k < U && v <= theta;
+        const unsigned m = __ballot_sync(FULL, take);
+        if (m) {
+          const int leader = __ffs(m) - 1;
+          int b0 = 0;
+          if (lane == leader) b0 = atomicAdd(&hdr[1], __popc(m));
+          b0 = __shfl_sync(FULL, b0, leader);
+          if (take) {
+            const int r = b0 + __popc(m & lanemask_lt());
+            R[r] = list[k];
+            if (r < 32) rval[r] = v;
+          }
+        }
       }
     }
     __syncthreads();
@@ -572,9 +613,12 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
 
     // ---- phase 4: exact fp64 ranking of R, output (warp 0)
     if (warp == 0) {
-      WarpTopK<KeyD, KPL> ex;
-      exact_rank<KPL>(p, ex, R, nR, stage64, rcap64, x64, __ldg(p.xlogx + x), lane);
-      const bool diff = emit_row<KPL>(p, ex, x, xr, lane);
+      bool diff;
+      if (!(KPL == 1 && p.out_kl == nullptr && nR <= 32 && certify_row(p, R, rval, nR, am, x, xr, lane, diff))) {
+        WarpTopK<KeyD, KPL> ex;
+        exact_rank<KPL>(p, ex, R, nR, stage64, rcap64, x64, __ldg(p.xlogx + x), lane);
+        diff = emit_row<KPL>(p, ex, x, xr, lane);
+      }
       if (lane == 0) {
         acc_comp += (unsigned long long)U;
         acc_changed += diff ? 1ull : 0ull;
@@ -805,22 +849,30 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
     }
     const float theta = T + 2.f * p.band * am + fabsf(T) * 1e-6f;
 
-    // ---- phase 3: R in place at the front of the list
+    // ---- phase 3: R (ids and screened values) in place at the front of list / scores
     int nR = 0;
     for (int k0 = 0; k0 < U; k0 += 32) {
       const int k = k0 + lane;
-      const bool take = k < U && scores[k] <= theta;
+      const float v = k < U ? scores[k] : 0.f;
+      const bool take = k < U && v <= theta;
       const int y = take ? list[k] : 0;
       const unsigned m = __ballot_sync(FULL, take);
-      if (take) list[nR + __popc(m & lanemask_lt())] = y;
+      if (take) {
+        const int r = nR + __popc(m & lanemask_lt());
+        list[r] = y;
+        scores[r] = v;
+      }
       nR += __popc(m);
     }
     __syncwarp();
 
-    // ---- phase 4: exact fp64 ranking of R, output
-    WarpTopK<KeyD, KPL> ex;
-    exact_rank<KPL>(p, ex, list, nR, stage64, rcap64, x64, __ldg(p.xlogx + x), lane);
-    const bool diff = emit_row<KPL>(p, ex, x, xr, lane);
+    // ---- phase 4: certify the screened order, else rank R exactly in fp64
+    bool diff;
+    if (!(KPL == 1 && p.out_kl == nullptr && nR <= 32 && certify_row(p, list, scores, nR, am, x, xr, lane, diff))) {
+      WarpTopK<KeyD, KPL> ex;
+      exact_rank<KPL>(p, ex, list, nR, stage64, rcap64, x64, __ldg(p.xlogx + x), lane);
+      diff = emit_row<KPL>(p, ex, x, xr, lane);
+    }
     if (lane == 0) {
       acc_comp += (unsigned long long)U;
       acc_changed += diff ? 1ull : 0ull;
