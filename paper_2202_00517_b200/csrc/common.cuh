@@ -114,6 +114,22 @@ __device__ __forceinline__ Key warp_sort32(Key v, int lane) {
   return v;
 }
 
+// sort one key per lane descending across the warp
+template <class Key>
+__device__ __forceinline__ Key warp_sort32_desc(Key v, int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      Key o = v.shfl_xor(j);
+      bool up = (lane & k) != 0;  // the mirror image of warp_sort32's directions
+      bool lower = (lane & j) == 0;
+      v = (lower == up) ? kmin(v, o) : kmax(v, o);
+    }
+  }
+  return v;
+}
+
 // sort a bitonic sequence (one key per lane) ascending (5 exchanges)
 template <class Key>
 __device__ __forceinline__ Key warp_merge32(Key v, int lane) {

@@ -742,12 +742,19 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
           }
         }
       };
+      int nxt2[UNR1];
       load_group(0);
+#pragma unroll
+      for (int u = 0; u < UNR1; ++u) nxt2[u] = nxt[u];
+      if (32 * UNR1 < total) load_group(32 * UNR1);
       for (int e0 = 0; e0 < total; e0 += 32 * UNR1) {
         int id[UNR1];
 #pragma unroll
-        for (int u = 0; u < UNR1; ++u) id[u] = nxt[u];
-        if (e0 + 32 * UNR1 < total) load_group(e0 + 32 * UNR1);
+        for (int u = 0; u < UNR1; ++u) {
+          id[u] = nxt2[u];
+          nxt2[u] = nxt[u];
+        }
+        if (e0 + 64 * UNR1 < total) load_group(e0 + 64 * UNR1);  // two groups ahead
 #pragma unroll
         for (int u = 0; u < UNR1; ++u) {
           const int y = id[u];
@@ -840,12 +847,21 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
     for (int o = 16; o > 0; o >>= 1) am = fmaxf(am, __shfl_xor_sync(FULL, am, o));
     float T = __int_as_float(0x7f800000);
     if (rows * Q >= K) {  // otherwise the kept subset may hold fewer than K values
-      WarpTopK<KeyF, KPL> top;
-      top.init();
-      top.first(KeyF{best[0]}, lane);
+      if constexpr (KPL == 1) {
+        // the 32 smallest of {best0} u {best1}: best0 ascending, best1 descending
+        // (two independent networks), elementwise min, one bitonic merge
+        const KeyF a = warp_sort32(KeyF{best[0]}, lane);
+        const KeyF b = warp_sort32_desc(KeyF{best[1]}, lane);
+        const KeyF m = warp_merge32(kmin(a, b), lane);
+        T = m.shfl(K - 1).v;  // >= the K-th smallest screened value (U >= K)
+      } else {
+        WarpTopK<KeyF, KPL> top;
+        top.init();
+        top.first(KeyF{best[0]}, lane);
 #pragma unroll
-      for (int q = 1; q < Q; ++q) top.insert(KeyF{best[q]}, K, lane);
-      T = top.get(K - 1).v;  // >= the K-th smallest screened value (U >= K)
+        for (int q = 1; q < Q; ++q) top.insert(KeyF{best[q]}, K, lane);
+        T = top.get(K - 1).v;
+      }
     }
     const float theta = T + 2.f * p.band * am + fabsf(T) * 1e-6f;
 
