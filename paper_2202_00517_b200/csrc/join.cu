@@ -729,17 +729,15 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
 #pragma unroll
         for (int u = 0; u < UNR1; ++u) {
           const int e = e0 + u * 32 + lane;
-          nxt[u] = -1;
-          if (e < total) {
-            const int v = S[s];
-            nxt[u] = (j == 0) ? v : __ldg(p.F + (int64_t)v * K + (j - 1));
-          }
+          const bool in = e < total;
+          const int v = S[in ? s : 0];
+          const int f = __ldg(p.F + (int64_t)v * K + (j > 0 ? j - 1 : 0));
+          nxt[u] = in ? (j == 0 ? v : f) : -1;
           s += Gq;
           j += Gr;
-          if (j >= K1) {
-            j -= K1;
-            ++s;
-          }
+          const bool wrap = j >= K1;
+          j -= wrap ? K1 : 0;
+          s += wrap ? 1 : 0;
         }
       };
       int nxt2[UNR1];
@@ -764,26 +762,19 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
           bool isnew = false;
           unsigned b = hash_slot(y, shift + 2);  // 4-slot bucket (one int4 read)
           while (__any_sync(FULL, pending)) {
-            int claim = -1;
-            if (pending) {
-              const int4 v = reinterpret_cast<const int4 *>(table)[b];
-              const unsigned hit = (v.x == y) | (v.y == y) | (v.z == y) | (v.w == y);
-              const unsigned emp =
-                  (v.x == EMPTY) | ((v.y == EMPTY) << 1) | ((v.z == EMPTY) << 2) | ((v.w == EMPTY) << 3);
-              if (hit) {
-                pending = false;
-              } else if (emp) {
-                claim = (int)(b * 4) + __ffs(emp) - 1;
-                table[claim] = y;
-              } else {
-                b = (b + 1) & bmask;
-              }
-            }
+            const int4 v = reinterpret_cast<const int4 *>(table)[b];
+            const bool hit = (v.x == y) | (v.y == y) | (v.z == y) | (v.w == y);
+            const unsigned emp =
+                (v.x == EMPTY) | ((v.y == EMPTY) << 1) | ((v.z == EMPTY) << 2) | ((v.w == EMPTY) << 3);
+            const bool claims = pending && !hit && emp != 0u;
+            const int claim = (int)(b * 4) + __ffs(emp) - 1;
+            if (claims) table[claim] = y;
+            b = (pending && !hit && emp == 0u) ? ((b + 1) & bmask) : b;  // full bucket: probe on
+            pending = pending && !hit;
             __syncwarp();
-            if (claim >= 0 && table[claim] == y) {  // a loser re-reads the same bucket
-              pending = false;
-              isnew = true;
-            }
+            const bool won = claims && table[claim] == y;  // a loser re-reads the same bucket
+            isnew = isnew || won;
+            pending = pending && !won;
             __syncwarp();
           }
           const unsigned m = __ballot_sync(FULL, isnew);
@@ -825,15 +816,17 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
         cp_async_wait_0();
       }
       __syncwarp();
-      if (lane < nrow) {
+      {
+        const int rl = lane < nrow ? lane : 0;  // lanes past nrow recompute row 0, discarded
         float ce, ab;
         if constexpr (NV4 > 0)
-          screen_row_reg<NV4>(stage + buf * rows * ld + lane * ld, xreg, p.nonpos, ce, ab);
+          screen_row_reg<NV4>(stage + buf * rows * ld + rl * ld, xreg, p.nonpos, ce, ab);
         else
-          screen_row<NV4>(stage + buf * rows * ld + lane * ld, x32, ld, p.nonpos, ce, ab);
-        scores[k0 + lane] = ce;
-        am = fmaxf(am, ab);
-        float v = ce;
+          screen_row<NV4>(stage + buf * rows * ld + rl * ld, x32, ld, p.nonpos, ce, ab);
+        const bool in = lane < nrow;
+        if (in) scores[k0 + lane] = ce;
+        am = in ? fmaxf(am, ab) : am;
+        float v = in ? ce : __int_as_float(0x7f800000);
 #pragma unroll
         for (int q = 0; q < Q; ++q) {  // insertion into the sorted per-lane list
           const float lo_ = fminf(best[q], v);
