@@ -899,7 +899,7 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
 
 // bin the anchors of [lo, hi) by pre-dedup bound P = (K+c)(K+1): class i is
 // the first with P <= lim[i]; the last class (global-memory tables) takes the rest
-constexpr int MAXCLS = 5;
+constexpr int MAXCLS = 6;
 struct Lims {
   int64_t v[MAXCLS];
   int n;  // number of classes (the last one is unbounded)
@@ -1001,9 +1001,11 @@ static Plan make_plan(int64_t m, int d, int K, int max_indeg) {
   if (l1 < lstage) l1 = lstage;
   if (l1 < 9) l1 = 9;
   if (l1 > 12) l1 = 12;
-  int kind[MAXCLS] = {KIND_WARP, KIND_BLOCK128, KIND_BLOCK256};
-  int logH[MAXCLS] = {l1, l1 + 1, l1 + 3 < 15 ? l1 + 3 : 15};
-  int n = 3;
+  // measured on B200 at C3 (KNND_PLAN sweeps): warp / 128-thread blocks for two
+  // table sizes / 256-thread blocks up to 2^15 slots / global tables
+  int kind[MAXCLS] = {KIND_WARP, KIND_BLOCK128, KIND_BLOCK128, KIND_BLOCK256, KIND_BLOCK256};
+  int logH[MAXCLS] = {l1, l1 + 1, l1 + 2, l1 + 3 < 15 ? l1 + 3 : 15, 15};
+  int n = l1 + 3 < 15 ? 5 : 4;
   if (const char *env = getenv("KNND_PLAN")) {
     int k2[MAXCLS], l2[MAXCLS];
     const int n2 = parse_plan(env, k2, l2);
