@@ -516,6 +516,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     // ---- phase 2: fp32 screen, one staged batch of rows per warp at a time
     float *scores = reinterpret_cast<float *>(table);  // the hash table is dead now
     float mn = __int_as_float(0x7f800000), mx = -mn, am = 0.f;
+    float best0 = mn, best1 = mn;  // this lane's two smallest screened values
     if (warp * wrows < U) {
       stage_rows_f32<NV4>(wstage, p.log32, list + warp * wrows, min(wrows, U - warp * wrows), ld, lane);
       cp_async_commit();
@@ -531,58 +532,89 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
         cp_async_wait_0();
       }
       __syncwarp();
-      if (lane < nrow) {
+      const int rr = (lane - ((k0 / wrows) * wrows)) & 31;  // rotate lanes across batches
+      if (rr < nrow) {
         float ce, ab;
-        screen_row<NV4>(wstage + buf * wrows * ld + lane * ld, x32, ld, p.nonpos, ce, ab);
-        scores[k0 + lane] = ce;
+        screen_row<NV4>(wstage + buf * wrows * ld + rr * ld, x32, ld, p.nonpos, ce, ab);
+        scores[k0 + rr] = ce;
         mn = fminf(mn, ce);
         mx = fmaxf(mx, ce);
         am = fmaxf(am, ab);
+        const float lo_ = fminf(best0, ce);
+        best1 = fminf(best1, fmaxf(best0, ce));
+        best0 = lo_;
       }
       __syncwarp();
     }
+    float T;
+    if constexpr (KPL == 1) {
+      // T >= the K-th smallest ce: each warp takes the 32 smallest of its lanes'
+      // two smallest (asc/desc networks + merge), warp 0 merges the W lists
+      const KeyF a = warp_sort32(KeyF{best0}, lane);
+      const KeyF b = warp_sort32_desc(KeyF{best1}, lane);
+      const KeyF m = warp_merge32(kmin(a, b), lane);
+      float *mlist = reinterpret_cast<float *>(hist);  // W x 32 floats (histograms unused here)
+      mlist[warp * 32 + lane] = m.v;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      mn = fminf(mn, __shfl_xor_sync(FULL, mn, o));
-      mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
-      am = fmaxf(am, __shfl_xor_sync(FULL, am, o));
-    }
-    if (lane == 0) {
-      red[warp * 4 + 0] = mn;
-      red[warp * 4 + 1] = mx;
-      red[warp * 4 + 2] = am;
-    }
-    __syncthreads();
+      for (int o = 16; o > 0; o >>= 1) am = fmaxf(am, __shfl_xor_sync(FULL, am, o));
+      if (lane == 0) red[warp * 4 + 2] = am;
+      __syncthreads();
+      if (warp == 0) {
+        KeyF acc{mlist[lane]};
+        for (int w = 1; w < W; ++w) acc = warp_merge32(kmin(acc, KeyF{mlist[w * 32 + 31 - lane]}), lane);
+        const float t = acc.shfl(K - 1).v;
+        if (lane == 0) reinterpret_cast<float *>(hdr)[2] = t;
+      }
+      __syncthreads();
+      T = reinterpret_cast<const float *>(hdr)[2];
 #pragma unroll
-    for (int w = 0; w < W; ++w) {
-      mn = fminf(mn, red[w * 4 + 0]);
-      mx = fmaxf(mx, red[w * 4 + 1]);
-      am = fmaxf(am, red[w * 4 + 2]);
-    }
+      for (int w = 0; w < W; ++w) am = fmaxf(am, red[w * 4 + 2]);
+      if (U < K) T = __int_as_float(0x7f800000);
+    } else {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        mn = fminf(mn, __shfl_xor_sync(FULL, mn, o));
+        mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
+        am = fmaxf(am, __shfl_xor_sync(FULL, am, o));
+      }
+      if (lane == 0) {
+        red[warp * 4 + 0] = mn;
+        red[warp * 4 + 1] = mx;
+        red[warp * 4 + 2] = am;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        mn = fminf(mn, red[w * 4 + 0]);
+        mx = fmaxf(mx, red[w * 4 + 1]);
+        am = fmaxf(am, red[w * 4 + 2]);
+      }
 
-    // ---- phase 2b: T >= the K-th smallest ce (two histogram passes)
-    float T = mx;
-    const float range = mx - mn;
-    if (U > 2 * K && range > 0.f) {
-      const float inv = (float)NBIN / range;
-      for (int k = tid; k < U; k += G) {
-        const float t = (scores[k] - mn) * inv;
-        atomicAdd(&hist[min(NBIN - 1, (int)t)], 1);
+      // T >= the K-th smallest ce (two histogram passes)
+      T = mx;
+      const float range = mx - mn;
+      if (U > 2 * K && range > 0.f) {
+        const float inv = (float)NBIN / range;
+        for (int k = tid; k < U; k += G) {
+          const float t = (scores[k] - mn) * inv;
+          atomicAdd(&hist[min(NBIN - 1, (int)t)], 1);
+        }
+        __syncthreads();
+        if (warp == 0) hist_find(hist, K, hdr, 2, lane);
+        __syncthreads();
+        const int b1 = hdr[2], before = hdr[3];
+        for (int k = tid; k < U; k += G) {
+          const float t = (scores[k] - mn) * inv;
+          if (min(NBIN - 1, (int)t) == b1)
+            atomicAdd(&hist2[min(NBIN - 1, (int)((t - (float)b1) * (float)NBIN))], 1);
+        }
+        __syncthreads();
+        if (warp == 0) hist_find(hist2, K - before, hdr, 4, lane);
+        __syncthreads();
+        const int b2 = hdr[4];
+        T = mn + ((float)b1 + (float)(b2 + 1) * (1.0f / NBIN)) / inv;
+        T += (fabsf(T) + range) * 1e-6f;  // covers the rounding of t and of this line
       }
-      __syncthreads();
-      if (warp == 0) hist_find(hist, K, hdr, 2, lane);
-      __syncthreads();
-      const int b1 = hdr[2], before = hdr[3];
-      for (int k = tid; k < U; k += G) {
-        const float t = (scores[k] - mn) * inv;
-        if (min(NBIN - 1, (int)t) == b1) atomicAdd(&hist2[min(NBIN - 1, (int)((t - (float)b1) * (float)NBIN))], 1);
-      }
-      __syncthreads();
-      if (warp == 0) hist_find(hist2, K - before, hdr, 4, lane);
-      __syncthreads();
-      const int b2 = hdr[4];
-      T = mn + ((float)b1 + (float)(b2 + 1) * (1.0f / NBIN)) / inv;
-      T += (fabsf(T) + range) * 1e-6f;  // covers the rounding of t and of this line
     }
     const float theta = T + 2.f * p.band * am + fabsf(T) * 1e-6f;
 
@@ -817,14 +849,18 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
       }
       __syncwarp();
       {
-        const int rl = lane < nrow ? lane : 0;  // lanes past nrow recompute row 0, discarded
+        // rotate the lanes that take this batch's rows, so every lane's two
+        // smallest cover its share of U even when a batch holds < 32 rows
+        const int rot = rows < 24 ? (k0 & 31) : 0;  // (k0 is a multiple of rows)
+        const int rr = (lane - rot) & 31;
+        const bool in = rr < nrow;
+        const int rl = in ? rr : 0;  // lanes past nrow recompute row 0, discarded
         float ce, ab;
         if constexpr (NV4 > 0)
           screen_row_reg<NV4>(stage + buf * rows * ld + rl * ld, xreg, p.nonpos, ce, ab);
         else
           screen_row<NV4>(stage + buf * rows * ld + rl * ld, x32, ld, p.nonpos, ce, ab);
-        const bool in = lane < nrow;
-        if (in) scores[k0 + lane] = ce;
+        if (in) scores[k0 + rl] = ce;
         am = in ? fmaxf(am, ab) : am;
         float v = in ? ce : __int_as_float(0x7f800000);
 #pragma unroll
