@@ -285,7 +285,7 @@ def b200_arm(args):
     # ---- end to end through the public API from host buffers
     e2e_s, e2e_comps = 0.0, 0
     h2d = d2h = 0
-    for i in range(args.e2e_steps + 1):
+    for i in range(args.e2e_steps + 1 if args.e2e_steps > 0 else 0):
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
