@@ -517,34 +517,60 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     float *scores = reinterpret_cast<float *>(table);  // the hash table is dead now
     float mn = __int_as_float(0x7f800000), mx = -mn, am = 0.f;
     float best0 = mn, best1 = mn;  // this lane's two smallest screened values
-    if (warp * wrows < U) {
-      stage_rows_f32<NV4>(wstage, p.log32, list + warp * wrows, min(wrows, U - warp * wrows), ld, lane);
-      cp_async_commit();
+    float4 xreg[NV4 > 0 ? NV4 : 1];  // the anchor's fp32 row in registers
+    if constexpr (NV4 > 0) {
+#pragma unroll
+      for (int q = 0; q < NV4; ++q) xreg[q] = reinterpret_cast<const float4 *>(x32)[q];
     }
-    for (int k0 = warp * wrows, buf = 0; k0 < U; k0 += W * wrows, buf ^= 1) {
-      const int nrow = min(wrows, U - k0);
-      const int k1 = k0 + W * wrows;
-      if (k1 < U) {  // prefetch this warp's next batch into the other buffer
-        stage_rows_f32<NV4>(wstage + (buf ^ 1) * wrows * ld, p.log32, list + k1, min(wrows, U - k1), ld, lane);
+    {
+      // this warp's batches: k0 = warp*wrows + it*W*wrows; lane r holds the id of
+      // row r of the batch being staged (ids of the batch after that in id_after)
+      const int kstep = W * wrows;
+      int k0 = warp * wrows;
+      int id_next = (k0 < U && lane < wrows && k0 + lane < U) ? list[k0 + lane] : 0;
+      int id_after = (k0 + kstep < U && lane < wrows && k0 + kstep + lane < U) ? list[k0 + kstep + lane] : 0;
+      if (k0 < U) {
+        if constexpr (NV4 > 0)
+          stage_rows_f32_reg<NV4>(wstage, p.log32, id_next, min(wrows, U - k0), lane);
+        else
+          stage_rows_f32<NV4>(wstage, p.log32, list + k0, min(wrows, U - k0), ld, lane);
         cp_async_commit();
-        cp_async_wait_1();
-      } else {
-        cp_async_wait_0();
       }
-      __syncwarp();
-      const int rr = (lane - ((k0 / wrows) * wrows)) & 31;  // rotate lanes across batches
-      if (rr < nrow) {
+      for (int buf = 0; k0 < U; k0 += kstep, buf ^= 1) {
+        const int nrow = min(wrows, U - k0);
+        const int k1 = k0 + kstep;
+        if (k1 < U) {  // prefetch this warp's next batch into the other buffer
+          if constexpr (NV4 > 0)
+            stage_rows_f32_reg<NV4>(wstage + (buf ^ 1) * wrows * ld, p.log32, id_after, min(wrows, U - k1), lane);
+          else
+            stage_rows_f32<NV4>(wstage + (buf ^ 1) * wrows * ld, p.log32, list + k1, min(wrows, U - k1), ld, lane);
+          cp_async_commit();
+          const int k2 = k1 + kstep;
+          id_after = (lane < wrows && k2 + lane < U) ? list[k2 + lane] : 0;
+          cp_async_wait_1();
+        } else {
+          cp_async_wait_0();
+        }
+        __syncwarp();
+        const int rr = (lane - k0) & 31;  // rotate lanes across batches (k0 is a multiple of wrows)
+        const bool in = rr < nrow;
+        const int rl = in ? rr : 0;
         float ce, ab;
-        screen_row<NV4>(wstage + buf * wrows * ld + rr * ld, x32, ld, p.nonpos, ce, ab);
-        scores[k0 + rr] = ce;
-        mn = fminf(mn, ce);
-        mx = fmaxf(mx, ce);
-        am = fmaxf(am, ab);
-        const float lo_ = fminf(best0, ce);
-        best1 = fminf(best1, fmaxf(best0, ce));
-        best0 = lo_;
+        if constexpr (NV4 > 0)
+          screen_row_reg<NV4>(wstage + buf * wrows * ld + rl * ld, xreg, p.nonpos, ce, ab);
+        else
+          screen_row<NV4>(wstage + buf * wrows * ld + rl * ld, x32, ld, p.nonpos, ce, ab);
+        if (in) {
+          scores[k0 + rl] = ce;
+          mn = fminf(mn, ce);
+          mx = fmaxf(mx, ce);
+          am = fmaxf(am, ab);
+          const float lo_ = fminf(best0, ce);
+          best1 = fminf(best1, fmaxf(best0, ce));
+          best0 = lo_;
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
     float T;
     if constexpr (KPL == 1) {
