@@ -782,15 +782,18 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
     int U = 0;
     {
       int s = s_init, j = j_init;
-      int nxt[UNR1];  // the next group of pre-dedup ids, loaded one group ahead
-      auto load_group = [&](int e0) {
+      // pre-dedup ids two groups ahead; the friend-row loads stay in flight until
+      // their group is consumed (the select below is deferred to that point)
+      int gf[2][UNR1], gv[2][UNR1], gm[2][UNR1];  // loaded friend id, S value, mode (0 out, 1 self, 2 friend)
+      auto load_group = [&](int slot, int e0) {
 #pragma unroll
         for (int u = 0; u < UNR1; ++u) {
           const int e = e0 + u * 32 + lane;
           const bool in = e < total;
           const int v = S[in ? s : 0];
-          const int f = __ldg(p.F + (int64_t)v * K + (j > 0 ? j - 1 : 0));
-          nxt[u] = in ? (j == 0 ? v : f) : -1;
+          gf[slot][u] = __ldg(p.F + (int64_t)v * K + (j > 0 ? j - 1 : 0));
+          gv[slot][u] = v;
+          gm[slot][u] = in ? (j == 0 ? 1 : 2) : 0;
           s += Gq;
           j += Gr;
           const bool wrap = j >= K1;
@@ -798,24 +801,23 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
           s += wrap ? 1 : 0;
         }
       };
-      int nxt2[UNR1];
-      load_group(0);
-#pragma unroll
-      for (int u = 0; u < UNR1; ++u) nxt2[u] = nxt[u];
-      if (32 * UNR1 < total) load_group(32 * UNR1);
-      for (int e0 = 0; e0 < total; e0 += 32 * UNR1) {
+      // one group: ids from slot `g` (a compile-time constant after inlining)
+      auto process = [&](const int g, const int e0) {
         int id[UNR1];
 #pragma unroll
+        for (int u = 0; u < UNR1; ++u) id[u] = gm[g][u] == 0 ? -1 : (gm[g][u] == 1 ? gv[g][u] : gf[g][u]);
+        if (e0 + 64 * UNR1 < total) load_group(g, e0 + 64 * UNR1);  // two groups ahead
+        unsigned grps[UNR1];  // in-batch duplicates, all four MATCHes issued together
+#pragma unroll
         for (int u = 0; u < UNR1; ++u) {
-          id[u] = nxt2[u];
-          nxt2[u] = nxt[u];
+          const bool valid = id[u] >= 0 && id[u] != x;
+          grps[u] = __match_any_sync(FULL, valid ? id[u] : -1 - lane);
         }
-        if (e0 + 64 * UNR1 < total) load_group(e0 + 64 * UNR1);  // two groups ahead
 #pragma unroll
         for (int u = 0; u < UNR1; ++u) {
           const int y = id[u];
           const bool valid = y >= 0 && y != x;
-          const unsigned grp = __match_any_sync(FULL, valid ? y : -1 - lane);
+          const unsigned grp = grps[u];
           bool pending = valid && (__ffs(grp) - 1 == lane);
           bool isnew = false;
           unsigned b = hash_slot(y, shift + 2);  // 4-slot bucket (one int4 read)
@@ -839,6 +841,12 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
           if (isnew) list[U + __popc(m & lanemask_lt())] = y;
           U += __popc(m);
         }
+      };
+      load_group(0, 0);
+      if (32 * UNR1 < total) load_group(1, 32 * UNR1);
+      for (int e0 = 0; e0 < total; e0 += 64 * UNR1) {
+        process(0, e0);
+        if (e0 + 32 * UNR1 < total) process(1, e0 + 32 * UNR1);
       }
     }
     __syncwarp();
