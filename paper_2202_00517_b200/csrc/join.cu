@@ -456,14 +456,19 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
   const int s_init = tid / K1, j_init = tid % K1;
   unsigned long long acc_comp = 0, acc_changed = 0, acc_bad = 0;
   const int count = *acount;
+  int *cursor = const_cast<int *>(acount) + 8;  // dynamic anchor fetch (zeroed with the counts)
+  if (tid == 0) hdr[8] = atomicAdd(cursor, 1);
+  __syncthreads();
 
-  for (int a = blockIdx.x; a < count; a += gridDim.x) {
+  for (int a = hdr[8]; a < count; a = hdr[8]) {
     const int x = alist[a];
     const int64_t xr = (int64_t)x - p.lo;
     const int64_t c0 = p.indptr[xr];
     const int c = (int)(p.indptr[xr + 1] - c0);
     const int nS = K + c;
     const int total = nS * K1;
+    __syncthreads();  // everyone has read hdr[8]
+    if (tid == 0) hdr[8] = atomicAdd(cursor, 1);  // the next anchor, published by a later barrier
 
     // ---- phase 0: clear table + histograms, stage S and the anchor row
     {
@@ -753,9 +758,19 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
   const int s_init = lane / K1, j_init = lane % K1;
   unsigned long long acc_comp = 0, acc_changed = 0, acc_bad = 0;
   const int count = *acount;
-  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  int *cursor = const_cast<int *>(acount) + 8;  // dynamic anchor fetch, 4 anchors per atomic
+  int a_base = 0, a_left = 0;
 
-  for (int a = blockIdx.x * (blockDim.x >> 5) + warp; a < count; a += nwarps) {
+  for (;;) {
+    if (a_left == 0) {
+      int got = 0;
+      if (lane == 0) got = atomicAdd(cursor, 4);
+      a_base = __shfl_sync(FULL, got, 0);
+      a_left = 4;
+    }
+    const int a = a_base++;
+    --a_left;
+    if (a >= count) break;
     const int x = alist[a];
     const int64_t xr = (int64_t)x - p.lo;
     const int64_t c0 = p.indptr[xr];

@@ -20,7 +20,7 @@ from oracle import native, port  # noqa: E402
 
 src = sys.argv[1]
 out = {}
-for name, size in (("c1", None), ("c2", 10_000), ("c3", 10_000)):
+for name, size in (("c1", None), ("c2", 10_000), ("c3", 10_000), ("c4", 10_000)):
     meta = json.load(open(os.path.join(src, name, "meta.json")))
     n, d, k, seed = meta["n"], meta["d"], meta["k"], meta["seed"]
     final = np.load(os.path.join(src, name, f"table_r{meta['rounds_used']:02d}.npy"))

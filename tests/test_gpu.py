@@ -358,3 +358,14 @@ def test_c3_trajectory(cuda, trajectories):
 
     pts, final = _trajectory_check(trajectories, "c3")
     _recall_check("c3", pts, final, load_json("recall.json"), 10_000)
+
+
+@pytest.mark.slow
+def test_c4_trajectory(cuda, trajectories):
+    """n=1M, d=50, K=30: hub anchors (in-degree up to 32,393) exercise every size class."""
+    from conftest import load_json
+
+    pts, final = _trajectory_check(trajectories, "c4")
+    rec = load_json("recall.json")
+    if "c4" in rec:
+        _recall_check("c4", pts, final, rec, 10_000)
