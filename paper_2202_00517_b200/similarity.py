@@ -83,7 +83,7 @@ class DeviceTables:
         self.xlogx = torch.empty((self.n,), dtype=torch.float64, device=device)
         self.h2d_bytes = host.numel() * 8
         # all coordinates <= 1 -> all logs <= 0 (lets the join skip one accumulator)
-        self.max_coord = float(points.max()) if points.size else 0.0
+        self.max_coord = float(self.points.max().item()) if points.size else 0.0
         _lib.call("knnd_kl_prepare", self.points.data_ptr(), self.n, self.d, self.ld, self.log32.data_ptr(),
                   self.log64.data_ptr(), self.xlogx.data_ptr(), _stream(device))
 
