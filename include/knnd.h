@@ -95,6 +95,11 @@ int knnd_csr_build(const int32_t *friends, int64_t n, int32_t k, int64_t row_lo,
  *   tally[2] += #anchors with |U_x| < K (malformed input; must stay 0)
  *   (tally is 4 x uint64, device memory, accumulated — the caller zeroes it)
  * max_indeg must be >= the longest CSR segment (from knnd_csr_build).
+ * bound_in / bound_out (nullable, row_hi-row_lo floats): a per-row bound kept
+ * between rounds — bound_out[x] receives the largest screened (fp32) value
+ * among the row written for x; passing it back as bound_in with the table
+ * built from those rows lets the next round skip the threshold selection.
+ * Use NaN (or NULL) when unknown; a bound from any other table is invalid.
  * flags: KNND_JOIN_NONPOS_LOG when every coordinate of every point is <= 1
  * (all logs <= 0, e.g. simplex data): the screen's error scale
  * sum |x log y| then equals -sum x log y and is not accumulated separately.
@@ -108,8 +113,8 @@ int knnd_local_join(const double *points, const float *log32, const double *log6
                     const int32_t *friends, int32_t k, const int64_t *indptr,
                     const int32_t *indices, int64_t row_lo, int64_t row_hi,
                     int32_t max_indeg, int32_t *out_ids, double *out_kl,
-                    int32_t *out_ucount, unsigned long long *tally, void *ws,
-                    size_t ws_bytes, uint32_t flags, void *stream);
+                    int32_t *out_ucount, unsigned long long *tally, const float *bound_in,
+                    float *bound_out, void *ws, size_t ws_bytes, uint32_t flags, void *stream);
 
 /*
  * Friend clustering rate count — friend_clustering_rate (descent.py:317-338)

@@ -36,7 +36,7 @@ _SIGS = {
     "knnd_csr_build": ([_P, _I64, _I32, _I64, _I64, _P, _P, _P, _P, _SZ, _P], C.c_int),
     "knnd_local_join_workspace_bytes": ([_I64, _I32, _I32, _I64, _I64, _I32], _SZ),
     "knnd_local_join": ([_P, _P, _P, _P, _I64, _I32, _I32, _P, _I32, _P, _P, _I64, _I64, _I32, _P, _P, _P, _P,
-                         _P, _SZ, C.c_uint32, _P], C.c_int),
+                         _P, _P, _P, _SZ, C.c_uint32, _P], C.c_int),
     "knnd_fcc": ([_P, _I64, _I32, _P, _P, _P, _I32, _P, _P], C.c_int),
     "knnd_sort_rows": ([_P, _P, _P, _I64, _I32, _I32, _I64, _I64, _P, _P, _P, _P], C.c_int),
     "knnd_random_kout_workspace_bytes": ([_I64, _I32], _SZ),

@@ -57,6 +57,8 @@ struct JoinParams {
   int d, ld, K;
   float band;
   int nonpos;  // every log coordinate <= 0: sum |x log y| == -sum x log y exactly
+  const float *__restrict__ bound_in;  // per own row: max screened value of the current row (or NaN)
+  float *__restrict__ bound_out;       // the same for the row written this round
 };
 
 __host__ __device__ inline size_t al16(size_t v) { return (v + 15) & ~(size_t)15; }
@@ -314,7 +316,7 @@ __device__ __forceinline__ void exact_rank(const JoinParams &p, WarpTopK<KeyD, K
 // top K+1 — hence the row — is the screened order (exact ties are impossible
 // at that distance).  Returns false (nothing written) when a gap is too small.
 __device__ __forceinline__ bool certify_row(const JoinParams &p, const int32_t *ids, const float *vals, int nR,
-                                            float am, int x, int64_t xr, int lane, bool &diff) {
+                                            float am, int x, int64_t xr, int lane, bool &diff, float &kth) {
   const int K = p.K;
   KeyFI key = KeyFI::inf();
   if (lane < nR) key = {vals[lane], ids[lane]};
@@ -325,6 +327,7 @@ __device__ __forceinline__ bool certify_row(const JoinParams &p, const int32_t *
   const bool need_check = lane < K && lane + 1 < nR;  // nR == K: the set is R itself
   const bool ok = !need_check || (nextv - key.v > gap_need);
   if (!__all_sync(FULL, ok)) return false;
+  kth = __shfl_sync(FULL, key.v, K - 1);
   bool d = false;
   if (lane < K) {
     p.out_ids[xr * K + lane] = key.id;
@@ -677,11 +680,13 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     // ---- phase 4: exact fp64 ranking of R, output (warp 0)
     if (warp == 0) {
       bool diff;
-      if (!(KPL == 1 && p.out_kl == nullptr && nR <= 32 && certify_row(p, R, rval, nR, am, x, xr, lane, diff))) {
+      float kth = theta;  // every member of the new row has a screened value <= theta
+      if (!(KPL == 1 && p.out_kl == nullptr && nR <= 32 && certify_row(p, R, rval, nR, am, x, xr, lane, diff, kth))) {
         WarpTopK<KeyD, KPL> ex;
         exact_rank<KPL>(p, ex, R, nR, stage64, rcap64, x64, __ldg(p.xlogx + x), lane);
         diff = emit_row<KPL>(p, ex, x, xr, lane);
       }
+      if (p.bound_out && lane == 0) p.bound_out[xr] = kth;
       if (lane == 0) {
         acc_comp += (unsigned long long)U;
         acc_changed += diff ? 1ull : 0ull;
@@ -923,23 +928,43 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) am = fmaxf(am, __shfl_xor_sync(FULL, am, o));
-    float T = __int_as_float(0x7f800000);
-    if (rows * Q >= K) {  // otherwise the kept subset may hold fewer than K values
-      if constexpr (KPL == 1) {
-        // the 32 smallest of {best0} u {best1}: best0 ascending, best1 descending
-        // (two independent networks), elementwise min, one bitonic merge
-        const KeyF a = warp_sort32(KeyF{best[0]}, lane);
-        const KeyF b = warp_sort32_desc(KeyF{best[1]}, lane);
-        const KeyF m = warp_merge32(kmin(a, b), lane);
-        T = m.shfl(K - 1).v;  // >= the K-th smallest screened value (U >= K)
-      } else {
-        WarpTopK<KeyF, KPL> top;
-        top.init();
-        top.first(KeyF{best[0]}, lane);
+    // Threshold.  The previous round's bound of this row (the largest screened
+    // value among the current friends, all of which are in U) is a valid T; it
+    // is used when it admits at most 32 candidates, else T comes from the lanes'
+    // two smallest values.
+    auto lane_pair_T = [&]() -> float {
+      float t = __int_as_float(0x7f800000);
+      if (rows * Q >= K) {  // otherwise the kept subset may hold fewer than K values
+        if constexpr (KPL == 1) {
+          // the 32 smallest of {best0} u {best1}: best0 ascending, best1 descending
+          // (two independent networks), elementwise min, one bitonic merge
+          const KeyF a = warp_sort32(KeyF{best[0]}, lane);
+          const KeyF b = warp_sort32_desc(KeyF{best[1]}, lane);
+          const KeyF m = warp_merge32(kmin(a, b), lane);
+          t = m.shfl(K - 1).v;  // >= the K-th smallest screened value (U >= K)
+        } else {
+          WarpTopK<KeyF, KPL> top;
+          top.init();
+          top.first(KeyF{best[0]}, lane);
 #pragma unroll
-        for (int q = 1; q < Q; ++q) top.insert(KeyF{best[q]}, K, lane);
-        T = top.get(K - 1).v;
+          for (int q = 1; q < Q; ++q) top.insert(KeyF{best[q]}, K, lane);
+          t = top.get(K - 1).v;
+        }
       }
+      return t;
+    };
+    const float T0 = p.bound_in ? p.bound_in[xr] : __int_as_float(0x7fc00000);
+    float T;
+    if (KPL == 1 && isfinite(T0)) {
+      const float th0 = T0 + 2.f * p.band * am + fabsf(T0) * 1e-6f;
+      int cnt = 0;
+      for (int k0 = 0; k0 < U; k0 += 32) {
+        const int k = k0 + lane;
+        cnt += __popc(__ballot_sync(FULL, k < U && scores[k] <= th0));
+      }
+      T = cnt <= 32 ? T0 : lane_pair_T();
+    } else {
+      T = lane_pair_T();
     }
     const float theta = T + 2.f * p.band * am + fabsf(T) * 1e-6f;
 
@@ -962,11 +987,14 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
 
     // ---- phase 4: certify the screened order, else rank R exactly in fp64
     bool diff;
-    if (!(KPL == 1 && p.out_kl == nullptr && nR <= 32 && certify_row(p, list, scores, nR, am, x, xr, lane, diff))) {
+    float kth = theta;  // every member of the new row has a screened value <= theta
+    if (!(KPL == 1 && p.out_kl == nullptr && nR <= 32 &&
+          certify_row(p, list, scores, nR, am, x, xr, lane, diff, kth))) {
       WarpTopK<KeyD, KPL> ex;
       exact_rank<KPL>(p, ex, list, nR, stage64, rcap64, x64, __ldg(p.xlogx + x), lane);
       diff = emit_row<KPL>(p, ex, x, xr, lane);
     }
+    if (p.bound_out && lane == 0) p.bound_out[xr] = kth;
     if (lane == 0) {
       acc_comp += (unsigned long long)U;
       acc_changed += diff ? 1ull : 0ull;
@@ -1256,8 +1284,8 @@ size_t knnd_local_join_workspace_bytes(int64_t n, int32_t d, int32_t k, int64_t 
 int knnd_local_join(const double *points, const float *log32, const double *log64, const double *xlogx, int64_t n,
                     int32_t d, int32_t ld32, const int32_t *friends, int32_t k, const int64_t *indptr,
                     const int32_t *indices, int64_t row_lo, int64_t row_hi, int32_t max_indeg, int32_t *out_ids,
-                    double *out_kl, int32_t *out_ucount, unsigned long long *tally, void *ws, size_t ws_bytes,
-                    uint32_t flags, void *stream) {
+                    double *out_kl, int32_t *out_ucount, unsigned long long *tally, const float *bound_in,
+                    float *bound_out, void *ws, size_t ws_bytes, uint32_t flags, void *stream) {
   KNND_CHECK_ARG(points && log32 && log64 && xlogx && friends && indptr && indices && out_ids && tally,
                  "knnd_local_join: null pointer");
   KNND_CHECK_ARG(n >= 2 && d >= 1, "knnd_local_join: bad shape n=%lld d=%d", (long long)n, d);
@@ -1306,6 +1334,8 @@ int knnd_local_join(const double *points, const float *log32, const double *log6
   // rigorous bound on |fp32 screen - fp64| relative to sum |x*log y| (+ margin)
   p.band = (float)((ld32 + 8) * 0x1p-24);
   p.nonpos = (flags & KNND_JOIN_NONPOS_LOG) ? 1 : 0;
+  p.bound_in = bound_in;
+  p.bound_out = bound_out;
 
   KNND_CUDA(cudaMemsetAsync(counts, 0, 64, st));
   {

@@ -131,9 +131,11 @@ class KnnState:
         self._host = arr
 
     @classmethod
-    def _from_device(cls, eng: Engine, table, csr: Csr, max_indeg: int, round_index: int, hist) -> "KnnState":
+    def _from_device(cls, eng: Engine, table, csr: Csr, max_indeg: int, round_index: int, hist,
+                     bound=None) -> "KnnState":
         st = cls.__new__(cls)
         st._bind(eng, table, csr, max_indeg, round_index, tuple(hist))
+        st._bound = bound
         return st
 
     def _bind(self, eng, table, csr, max_indeg, round_index, hist):
@@ -145,6 +147,9 @@ class KnnState:
         self.fcc_history = hist
         self._host = None
         self._host_csr = None
+        # (tables, per-row bound) from the round that produced this table; a
+        # hint for the next join with the same tables, never shared or mutated
+        self._bound = None
 
     # -- reference attributes ----------------------------------------------
     @property
@@ -346,11 +351,13 @@ def _check_state(state: KnnState) -> None:
 
 def _round(state: KnnState, tabs, samples_dev, sample_count: int, round_index: int):
     eng = state._engine
-    nxt, res = eng.round(tabs, state._table, state._csr, state._max_indeg, samples_dev)
+    bound = state._bound[1] if state._bound is not None and state._bound[0] is tabs else None
+    nxt, res = eng.round(tabs, state._table, state._csr, state._max_indeg, samples_dev, bound=bound)
     if res.bad:
         raise RuntimeError(f"local join saw {res.bad} anchors with fewer than K candidates (malformed table)")
     rate = res.fcc_count / sample_count
-    new_state = KnnState._from_device(eng, nxt, res.csr, res.max_indeg, round_index, state.fcc_history + (rate,))
+    new_state = KnnState._from_device(eng, nxt, res.csr, res.max_indeg, round_index, state.fcc_history + (rate,),
+                                      (tabs, res.bound))
     return new_state, res, rate
 
 

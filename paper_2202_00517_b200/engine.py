@@ -87,7 +87,8 @@ class CudaOps:
 
     def join(self, tabs, table: torch.Tensor, n: int, k: int, csr: Csr, max_indeg: int, out_rows: torch.Tensor,
              tally: torch.Tensor, out_kl: torch.Tensor | None = None, out_ucount: torch.Tensor | None = None,
-             flags: int | None = None) -> None:
+             flags: int | None = None, bound_in: torch.Tensor | None = None,
+             bound_out: torch.Tensor | None = None) -> None:
         if flags is None:
             flags = _lib.JOIN_NONPOS_LOG if tabs.max_coord <= 1.0 else 0
         nbytes = _lib.load().knnd_local_join_workspace_bytes(n, tabs.d, k, csr.lo, csr.hi, max_indeg)
@@ -96,8 +97,10 @@ class CudaOps:
                   tabs.xlogx.data_ptr(), n, tabs.d, tabs.ld, table.data_ptr(), k, csr.indptr.data_ptr(),
                   csr.indices.data_ptr(), csr.lo, csr.hi, max_indeg, out_rows.data_ptr(),
                   out_kl.data_ptr() if out_kl is not None else None,
-                  out_ucount.data_ptr() if out_ucount is not None else None, tally.data_ptr(), ws.data_ptr(),
-                  ws.numel(), flags, self._stream())
+                  out_ucount.data_ptr() if out_ucount is not None else None, tally.data_ptr(),
+                  bound_in.data_ptr() if bound_in is not None else None,
+                  bound_out.data_ptr() if bound_out is not None else None, ws.data_ptr(), ws.numel(), flags,
+                  self._stream())
 
     def random_kout(self, state: tuple, n: int, k: int, table: torch.Tensor, out_meta: torch.Tensor,
                     bad: torch.Tensor) -> None:
@@ -131,6 +134,7 @@ class RoundResult:
     bad: int
     fcc_count: int
     max_indeg: int
+    bound: torch.Tensor | None = None  # per own row: largest screened value of the new row
 
 
 class Engine:
@@ -207,23 +211,27 @@ class Engine:
         return table
 
     def round(self, tabs, table: torch.Tensor, csr: Csr, max_indeg: int, samples: torch.Tensor | None,
-              out_kl: torch.Tensor | None = None, out_ucount: torch.Tensor | None = None
-              ) -> tuple[torch.Tensor, RoundResult]:
+              out_kl: torch.Tensor | None = None, out_ucount: torch.Tensor | None = None,
+              bound: torch.Tensor | None = None) -> tuple[torch.Tensor, RoundResult]:
+        """One round.  `bound` is the RoundResult.bound of the round that produced
+        `table` with the same `tabs` (or None); the new one is returned."""
         tally = self.stats[0:4]
         tally.zero_()
         nxt = self.alloc_table()
+        s = self.shard
+        bound_out = torch.empty(max(s.hi - s.lo, 1), dtype=torch.float32, device=self.device)
         ev = None
         if self.join_events is not None:
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             ev[0].record()
-        self.ops.join(tabs, table, self.n, self.k, csr, max_indeg, self.own_rows(nxt), tally, out_kl, out_ucount)
+        self.ops.join(tabs, table, self.n, self.k, csr, max_indeg, self.own_rows(nxt), tally, out_kl, out_ucount,
+                      bound_in=bound, bound_out=bound_out)
         if ev is not None:
             ev[1].record()
         self.stats[5:6].copy_(tally[0:1])  # this rank's comparisons (before the all-reduce)
         if self.shard.world > 1:
             self.exchange(nxt)
             dist.all_reduce(tally, group=self.group)
-        s = self.shard
         csr_next = self.ops.csr(nxt, self.n, self.k, s.lo, s.hi, self._stats32[9:10])
         if samples is not None:
             self.ops.fcc(nxt, self.n, self.k, samples, self._stats32[8:9])
@@ -231,7 +239,8 @@ class Engine:
         h32 = host.view(torch.int32)
         if ev is not None:
             self.join_events.append((ev[0].elapsed_time(ev[1]), int(host[5])))
-        return nxt, RoundResult(csr_next, int(host[0]), int(host[1]), int(host[2]), int(h32[8]), int(h32[9]))
+        return nxt, RoundResult(csr_next, int(host[0]), int(host[1]), int(host[2]), int(h32[8]), int(h32[9]),
+                                bound_out)
 
     def fcc(self, table: torch.Tensor, samples: torch.Tensor) -> int:
         self.ops.fcc(table, self.n, self.k, samples, self._stats32[8:9])

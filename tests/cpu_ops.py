@@ -20,7 +20,10 @@ class CpuOps:
             max_out[0] = int(np.diff(ptr[lo:hi + 1]).max()) if hi > lo else 0
         return Csr(torch.from_numpy(sub_ptr.copy()), torch.from_numpy(sub_idx), lo, hi)
 
-    def join(self, tabs, table, n, k, csr, max_indeg, out_rows, tally, out_kl=None, out_ucount=None):
+    def join(self, tabs, table, n, k, csr, max_indeg, out_rows, tally, out_kl=None, out_ucount=None, flags=None,
+             bound_in=None, bound_out=None):
+        if bound_out is not None:
+            bound_out.fill_(float("nan"))  # no bound: the device kernel treats NaN as unknown
         full_ptr = np.zeros(n + 1, np.int64)
         full_ptr[csr.lo:csr.hi + 1] = csr.indptr.numpy()
         rows, kl, uc, comps, changed = native.local_join(tabs, table[:n].numpy(), np.arange(csr.lo, csr.hi),

@@ -64,7 +64,7 @@ def test_workspace_queries(lib):
 def test_argument_errors_are_reported(lib):
     null = None
     rc = lib.knnd_local_join(null, null, null, null, 10, 4, 4, null, 3, null, null, 0, 10, 5, null, null, null,
-                             null, null, 0, 0, null)
+                             null, null, null, null, 0, 0, null)
     assert rc == -1 and "null" in _lib.last_error()
     rc = lib.knnd_csr_build(C.c_void_p(16), 10, 3, 5, 2, C.c_void_p(16), C.c_void_p(16), null, C.c_void_p(16), 1 << 20,
                             null)
