@@ -79,65 +79,64 @@ struct KeyD {
   }
 };
 
-// screened value with its id (the order used to certify a row without fp64)
-struct KeyFI {
-  float v;
-  int id;
-  __device__ __forceinline__ static KeyFI inf() { return {__int_as_float(0x7f800000), 0x7fffffff}; }
-  __device__ __forceinline__ bool lt(const KeyFI &o) const { return v < o.v || (v == o.v && id < o.id); }
-  __device__ __forceinline__ KeyFI shfl(int src) const {
-    return {__shfl_sync(FULL, v, src), __shfl_sync(FULL, id, src)};
-  }
-  __device__ __forceinline__ KeyFI shfl_xor(int m) const {
-    return {__shfl_xor_sync(FULL, v, m), __shfl_xor_sync(FULL, id, m)};
-  }
-};
-
 template <class Key>
 __device__ __forceinline__ Key kmin(const Key &a, const Key &b) { return b.lt(a) ? b : a; }
 template <class Key>
 __device__ __forceinline__ Key kmax(const Key &a, const Key &b) { return a.lt(b) ? b : a; }
 
-// sort one key per lane ascending across the warp (bitonic, 15 exchanges)
+// One bitonic compare-exchange with the partner lane (lane ^ j): keep the
+// smaller key, or the larger when keep_max — one comparison, one select.
+// (screened value, id) packed into one orderable 64-bit integer: the same
+// order as (value, id) lexicographic with a single 64-bit comparison (used to
+// certify a row without fp64)
+struct KeyU {
+  unsigned long long k;
+  __device__ __forceinline__ static unsigned ord(float f) {
+    const unsigned b = __float_as_uint(f);
+    return b ^ ((unsigned)((int)b >> 31) | 0x80000000u);
+  }
+  __device__ __forceinline__ static KeyU make(float v, int id) {
+    return {((unsigned long long)ord(v) << 32) | (unsigned)id};
+  }
+  __device__ __forceinline__ static KeyU inf() { return make(__int_as_float(0x7f800000), 0x7fffffff); }
+  __device__ __forceinline__ float v() const {
+    const unsigned u = (unsigned)(k >> 32);
+    return __uint_as_float(u ^ ((unsigned)((int)~u >> 31) | 0x80000000u));
+  }
+  __device__ __forceinline__ int id() const { return (int)(unsigned)k; }
+  __device__ __forceinline__ bool lt(const KeyU &o) const { return k < o.k; }
+  __device__ __forceinline__ KeyU shfl(int src) const { return {__shfl_sync(FULL, k, src)}; }
+  __device__ __forceinline__ KeyU shfl_xor(int m) const { return {__shfl_xor_sync(FULL, k, m)}; }
+};
+
 template <class Key>
+__device__ __forceinline__ Key cmpx(Key v, int j, bool keep_max) {
+  const Key o = v.shfl_xor(j);
+  return (o.lt(v) != keep_max) ? o : v;
+}
+
+// sort one key per lane ascending (desc: descending) across the warp
+// (bitonic, 15 exchanges)
+template <class Key, bool DESC = false>
 __device__ __forceinline__ Key warp_sort32(Key v, int lane) {
 #pragma unroll
   for (int k = 2; k <= 32; k <<= 1) {
 #pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      Key o = v.shfl_xor(j);
-      bool up = (lane & k) == 0;
-      bool lower = (lane & j) == 0;
-      v = (lower == up) ? kmin(v, o) : kmax(v, o);
-    }
+    for (int j = k >> 1; j > 0; j >>= 1) v = cmpx(v, j, (((lane & k) != 0) != ((lane & j) != 0)) != DESC);
   }
   return v;
 }
 
-// sort one key per lane descending across the warp
 template <class Key>
 __device__ __forceinline__ Key warp_sort32_desc(Key v, int lane) {
-#pragma unroll
-  for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      Key o = v.shfl_xor(j);
-      bool up = (lane & k) != 0;  // the mirror image of warp_sort32's directions
-      bool lower = (lane & j) == 0;
-      v = (lower == up) ? kmin(v, o) : kmax(v, o);
-    }
-  }
-  return v;
+  return warp_sort32<Key, true>(v, lane);
 }
 
 // sort a bitonic sequence (one key per lane) ascending (5 exchanges)
 template <class Key>
 __device__ __forceinline__ Key warp_merge32(Key v, int lane) {
 #pragma unroll
-  for (int j = 16; j > 0; j >>= 1) {
-    Key o = v.shfl_xor(j);
-    v = ((lane & j) == 0) ? kmin(v, o) : kmax(v, o);
-  }
+  for (int j = 16; j > 0; j >>= 1) v = cmpx(v, j, (lane & j) != 0);
   return v;
 }
 

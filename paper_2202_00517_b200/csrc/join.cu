@@ -318,20 +318,21 @@ __device__ __forceinline__ void exact_rank(const JoinParams &p, WarpTopK<KeyD, K
 __device__ __forceinline__ bool certify_row(const JoinParams &p, const int32_t *ids, const float *vals, int nR,
                                             float am, int x, int64_t xr, int lane, bool &diff, float &kth) {
   const int K = p.K;
-  KeyFI key = KeyFI::inf();
-  if (lane < nR) key = {vals[lane], ids[lane]};
+  KeyU key = KeyU::inf();
+  if (lane < nR) key = KeyU::make(vals[lane], ids[lane]);
   key = warp_sort32(key, lane);
-  const float nextv = __shfl_down_sync(FULL, key.v, 1);
+  const float kv = key.v();
+  const float nextv = __shfl_down_sync(FULL, kv, 1);
   const float band = 2.f * p.band * am;
-  const float gap_need = band + fabsf(key.v) * 2e-6f + 1e-30f;
+  const float gap_need = band + fabsf(kv) * 2e-6f + 1e-30f;
   const bool need_check = lane < K && lane + 1 < nR;  // nR == K: the set is R itself
-  const bool ok = !need_check || (nextv - key.v > gap_need);
+  const bool ok = !need_check || (nextv - kv > gap_need);
   if (!__all_sync(FULL, ok)) return false;
-  kth = __shfl_sync(FULL, key.v, K - 1);
+  kth = __shfl_sync(FULL, kv, K - 1);
   bool d = false;
   if (lane < K) {
-    p.out_ids[xr * K + lane] = key.id;
-    d = key.id != __ldg(p.F + (int64_t)x * K + lane);
+    p.out_ids[xr * K + lane] = key.id();
+    d = key.id() != __ldg(p.F + (int64_t)x * K + lane);
   }
   diff = __any_sync(FULL, d);
   return true;
@@ -743,7 +744,7 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
   extern __shared__ __align__(16) unsigned char sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int H = 1 << logH;
-  const unsigned shift = 32u - (unsigned)logH, bmask = ((unsigned)H >> 2) - 1u;
+  const unsigned shift = 32u - (unsigned)logH;
   const WarpSlab L = warp_slab(p.d, p.ld, H, SW);
   unsigned char *base = sm + (size_t)warp * (GLIST ? L.list : L.total);  // GLIST: no list in smem
   float *x32 = reinterpret_cast<float *>(base + L.x32);
@@ -798,7 +799,7 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
       for (int q = 0; q < NV4; ++q) xreg[q] = reinterpret_cast<const float4 *>(x32)[q];
     }
 
-    // ---- phase 1: dedup (no atomics)
+    // ---- phase 1: dedup
     int U = 0;
     {
       int s = s_init, j = j_init;
@@ -827,38 +828,16 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
 #pragma unroll
         for (int u = 0; u < UNR1; ++u) id[u] = gm[g][u] == 0 ? -1 : (gm[g][u] == 1 ? gv[g][u] : gf[g][u]);
         if (e0 + 64 * UNR1 < total) load_group(g, e0 + 64 * UNR1);  // two groups ahead
-        unsigned grps[UNR1];  // in-batch duplicates, all four MATCHes issued together
+        // shared-memory CAS insert (hash_insert_cas): in-warp duplicates resolve in
+        // the CAS itself; the ballots append the winners in lane order
+        bool nw[UNR1];
+#pragma unroll
+        for (int u = 0; u < UNR1; ++u)
+          nw[u] = id[u] >= 0 && id[u] != x && hash_insert_cas(table, id[u], shift, (unsigned)H - 1u);
 #pragma unroll
         for (int u = 0; u < UNR1; ++u) {
-          const bool valid = id[u] >= 0 && id[u] != x;
-          grps[u] = __match_any_sync(FULL, valid ? id[u] : -1 - lane);
-        }
-#pragma unroll
-        for (int u = 0; u < UNR1; ++u) {
-          const int y = id[u];
-          const bool valid = y >= 0 && y != x;
-          const unsigned grp = grps[u];
-          bool pending = valid && (__ffs(grp) - 1 == lane);
-          bool isnew = false;
-          unsigned b = hash_slot(y, shift + 2);  // 4-slot bucket (one int4 read)
-          while (__any_sync(FULL, pending)) {
-            const int4 v = reinterpret_cast<const int4 *>(table)[b];
-            const bool hit = (v.x == y) | (v.y == y) | (v.z == y) | (v.w == y);
-            const unsigned emp =
-                (v.x == EMPTY) | ((v.y == EMPTY) << 1) | ((v.z == EMPTY) << 2) | ((v.w == EMPTY) << 3);
-            const bool claims = pending && !hit && emp != 0u;
-            const int claim = (int)(b * 4) + __ffs(emp) - 1;
-            if (claims) table[claim] = y;
-            b = (pending && !hit && emp == 0u) ? ((b + 1) & bmask) : b;  // full bucket: probe on
-            pending = pending && !hit;
-            __syncwarp();
-            const bool won = claims && table[claim] == y;  // a loser re-reads the same bucket
-            isnew = isnew || won;
-            pending = pending && !won;
-            __syncwarp();
-          }
-          const unsigned m = __ballot_sync(FULL, isnew);
-          if (isnew) list[U + __popc(m & lanemask_lt())] = y;
+          const unsigned m = __ballot_sync(FULL, nw[u]);
+          if (nw[u]) list[U + __popc(m & lanemask_lt())] = id[u];
           U += __popc(m);
         }
       };
@@ -1347,11 +1326,38 @@ int knnd_local_join(const double *points, const float *log32, const double *log6
     classify_kernel<<<(unsigned)blocks, 256, 0, st>>>(indptr, m, row_lo, k, lims, lists, counts);
     KNND_LAUNCHED(1);
   }
+  // diagnostics: KNND_CLASS_TIMING=1 times each class (synchronising) and prints
+  // anchors / comparisons / ms per class to stderr
+  static const bool timing = getenv("KNND_CLASS_TIMING") != nullptr;
   // biggest tables first: the few long hub anchors start early
   for (int i = P.ncls - 1; i >= 0; --i) {
     if (!P.c[i].need) continue;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    unsigned long long t0[4] = {0, 0, 0, 0};
+    if (timing) {
+      KNND_CUDA(cudaStreamSynchronize(st));
+      KNND_CUDA(cudaMemcpy(t0, tally, sizeof(t0), cudaMemcpyDeviceToHost));
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, st);
+    }
     const int rc = dispatch_class(P, i, p, lists, counts, m, slabs, glists, st);
     if (rc) return rc;
+    if (timing) {
+      cudaEventRecord(e1, st);
+      KNND_CUDA(cudaStreamSynchronize(st));
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      unsigned long long t1[4];
+      int cnt[MAXCLS + 1];
+      KNND_CUDA(cudaMemcpy(t1, tally, sizeof(t1), cudaMemcpyDeviceToHost));
+      KNND_CUDA(cudaMemcpy(cnt, counts, sizeof(int) * P.ncls, cudaMemcpyDeviceToHost));
+      const unsigned long long u = t1[0] - t0[0];
+      fprintf(stderr, "knnd class %d kind %d logH %d: %d anchors, %llu comparisons, %.3f ms, %.3e/s\n", i,
+              P.c[i].kind, P.c[i].logH, cnt[i], u, ms, ms > 0 ? u / (ms * 1e-3) : 0.0);
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
   }
   return KNND_OK;
 }

@@ -3,7 +3,12 @@ import csv, subprocess, sys
 from collections import defaultdict
 
 rep = sys.argv[1]
-extra = sys.argv[3:]  # e.g. --launch-skip 1 --launch-count 1
+extra = sys.argv[3:]  # e.g. --launch-skip 1 --launch-count 1; "--col stall_no_inst" ranks by one stall reason
+col = None
+if "--col" in extra:
+    i = extra.index("--col")
+    col = extra[i + 1]
+    extra = extra[:i] + extra[i + 2:]
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass", *extra],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
@@ -17,7 +22,7 @@ for r in rows:
         continue
     if r and r[0] == "Line No":
         hdr = r
-        i_s = 4
+        i_s = hdr.index(col) if col else 4
         i_ex = hdr.index("Instructions Executed")
         continue
     if hdr is None or len(r) != len(hdr) or not r[0].isdigit() or r[2] != "-":
