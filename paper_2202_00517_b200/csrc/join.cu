@@ -448,9 +448,8 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     S = reinterpret_cast<int32_t *>(sm + L.S);
     table = reinterpret_cast<int32_t *>(sm + L.table);
     list = reinterpret_cast<int32_t *>(sm + L.list);
-    const int per_warp_floats = (H / 2) / W;  // upper half of the table, split over warps
-    wrows = min(32, per_warp_floats / (2 * p.ld));  // two buffers per warp
-    wstage = reinterpret_cast<float *>(table + H / 2) + (size_t)warp * per_warp_floats;
+    wrows = 0;  // set per anchor (the staging area follows the scores)
+    wstage = nullptr;
     stage64 = reinterpret_cast<double *>(table);  // lower half, free in phase 4
     rcap64 = min(32, (2 * H) / ((p.d | 1) * 8));
   }
@@ -524,6 +523,14 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
 
     // ---- phase 2: fp32 screen, one staged batch of rows per warp at a time
     float *scores = reinterpret_cast<float *>(table);  // the hash table is dead now
+    if constexpr (!GTAB) {
+      // staging: the table past the scores ([0, U), U <= H/2), split over warps,
+      // two buffers per warp
+      const int u4 = (U + 3) & ~3;
+      const int per_warp_floats = ((H - u4) / W) & ~3;
+      wrows = min(32, per_warp_floats / (2 * ld));
+      wstage = reinterpret_cast<float *>(table + u4) + (size_t)warp * per_warp_floats;
+    }
     float mn = __int_as_float(0x7f800000), mx = -mn, am = 0.f;
     float best0 = mn, best1 = mn;  // this lane's two smallest screened values
     float4 xreg[NV4 > 0 ? NV4 : 1];  // the anchor's fp32 row in registers
@@ -754,11 +761,9 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
   int32_t *list = GLIST ? glists + (size_t)(blockIdx.x * (blockDim.x >> 5) + warp) * (H >> 1)
                         : reinterpret_cast<int32_t *>(base + L.list);
   float *scores = reinterpret_cast<float *>(table);            // phase 2-3: [0, U)
-  float *stage = reinterpret_cast<float *>(table + (H >> 1));  // phase 2: upper half
   double *stage64 = reinterpret_cast<double *>(table);         // phase 4: whole table
   const int K = p.K, K1 = K + 1;
   const int d = p.d, ld = p.ld, sd = d | 1;
-  const int rows = min(32, (H / 2) / (ld * 2));  // two staging buffers in the table's upper half
   const int rcap64 = min(32, (4 * H) / (sd * 8));
   const int Gq = 32 / K1, Gr = 32 % K1;
   const int s_init = lane / K1, j_init = lane % K1;
@@ -856,6 +861,10 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
     for (int q = 0; q < Q; ++q) best[q] = __int_as_float(0x7f800000);
     float am = 0.f;
     // ids of batch b+1 are in a register while batch b computes; batch b+2's are being loaded
+    // two staging buffers in the table past the scores ([0, U), U <= H/2)
+    const int u4 = (U + 3) & ~3;
+    float *stage = reinterpret_cast<float *>(table + u4);
+    const int rows = min(32, (H - u4) / (ld * 2));
     int id_next = (lane < min(rows, U)) ? list[lane] : 0;
     int id_after = (rows + lane < U && lane < rows) ? list[rows + lane] : 0;
     if (U > 0) {
@@ -1178,20 +1187,29 @@ static int launch_warp(const JoinParams &p, const int32_t *alist, const int32_t 
   auto kern = join_warp_kernel<NV4, KPL, GLIST>;
   WarpSlab L = warp_slab(p.d, p.ld, 1 << logH, SW);
   if (GLIST) L.total = L.list;  // the unique list lives in the global slab
-  const size_t smem = L.total * (WARP_BLOCK / 32);
-  if (smem > 227 * 1024) {
-    set_error("local join: warp slabs %zu B exceed 227 KB (d=%d, H=%d)", smem, p.d, 1 << logH);
+  // warps per block: the largest of 4/2/1 that keeps the most warps resident
+  // (big tables leave room for fewer than 4 slabs per block slot)
+  int best_wpb = 0, best_warps = 0;
+  size_t smem = 0;
+  for (int wpb = WARP_BLOCK / 32; wpb >= 1; wpb >>= 1) {
+    const size_t sm_b = L.total * wpb;
+    if (sm_b > 227 * 1024) continue;
+    KNND_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_b));
+    int per_sm = 0;
+    KNND_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpb * 32, sm_b));
+    if (GLIST && per_sm * wpb > 64) per_sm = 64 / wpb;  // the workspace holds 64 warp lists per SM
+    if (per_sm * wpb > best_warps) {
+      best_warps = per_sm * wpb;
+      best_wpb = wpb;
+      smem = sm_b;
+    }
+  }
+  if (best_warps < 1) {
+    set_error("local join: warp slabs %zu B exceed 227 KB (d=%d, H=%d)", L.total, p.d, 1 << logH);
     return KNND_EUNSUPPORTED;
   }
   KNND_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  KNND_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARP_BLOCK, smem));
-  if (per_sm < 1) {
-    set_error("local join: warp kernel cannot be resident (smem=%zu)", smem);
-    return KNND_EUNSUPPORTED;
-  }
-  if (GLIST && per_sm > 16) per_sm = 16;  // the workspace holds 64 warp lists per SM
-  kern<<<per_sm * num_sms(), WARP_BLOCK, smem, st>>>(p, alist, acount, logH, SW, glists);
+  kern<<<(best_warps / best_wpb) * num_sms(), best_wpb * 32, smem, st>>>(p, alist, acount, logH, SW, glists);
   KNND_LAUNCHED(1);
   return KNND_OK;
 }
