@@ -341,6 +341,30 @@ __device__ __forceinline__ bool certify_row(const JoinParams &p, const int32_t *
 // ---------------------------------------------------------------------------
 // block-per-anchor kernel (classes B and L)
 
+// R = {k : scores[k] <= theta} (ids, and the screened values of the first 32)
+// appended block-wide through the counter *nr
+__device__ __forceinline__ void collect_r(const float *scores, const int32_t *list, int U, float theta, int32_t *R,
+                                          float *rval, int *nr, int tid, int lane, int G) {
+  const int iters = (U + G - 1) / G;
+  for (int it = 0; it < iters; ++it) {
+    const int k = it * G + tid;
+    const float v = k < U ? scores[k] : 0.f;
+    const bool take = k < U && v <= theta;
+    const unsigned m = __ballot_sync(FULL, take);
+    if (m) {
+      const int leader = __ffs(m) - 1;
+      int b0 = 0;
+      if (lane == leader) b0 = atomicAdd(nr, __popc(m));
+      b0 = __shfl_sync(FULL, b0, leader);
+      if (take) {
+        const int r = b0 + __popc(m & lanemask_lt());
+        R[r] = list[k];
+        if (r < 32) rval[r] = v;
+      }
+    }
+  }
+}
+
 struct SmemLayout {
   size_t x32, x64, red, hist, rval, stage, S, table, list, total;
 };
@@ -589,7 +613,34 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
       }
     }
     float T;
+    int32_t *R = table + (H >> 1);
+    bool collected = false;  // R already gathered (by the previous round's bound)
     if constexpr (KPL == 1) {
+      // The previous round's bound of this row is a valid T (all current friends
+      // are in U); with it, R is gathered in the same pass that counts it, and
+      // the threshold networks are skipped when it admits at most 32 candidates.
+      const float T0 = p.bound_in ? __ldg(p.bound_in + xr) : __int_as_float(0x7fc00000);
+      if (isfinite(T0) && U >= K) {
+        float aw = am;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) aw = fmaxf(aw, __shfl_xor_sync(FULL, aw, o));
+        if (lane == 0) red[warp * 4 + 2] = aw;
+        __syncthreads();  // every warp's scores and max |x log y|
+        float ab = 0.f;
+#pragma unroll
+        for (int w = 0; w < W; ++w) ab = fmaxf(ab, red[w * 4 + 2]);
+        const float th0 = T0 + 2.f * p.band * ab + fabsf(T0) * 1e-6f;
+        collect_r(scores, list, U, th0, R, rval, &hdr[1], tid, lane, G);
+        __syncthreads();
+        if (hdr[1] <= 32) {
+          T = T0;
+          am = ab;
+          collected = true;
+        }
+      }
+    }
+    if (collected) {
+    } else if constexpr (KPL == 1) {
       // T >= the K-th smallest ce: each warp takes the 32 smallest of its lanes'
       // two smallest (asc/desc networks + merge), warp 0 merges the W lists
       const KeyF a = warp_sort32(KeyF{best0}, lane);
@@ -605,7 +656,10 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
         KeyF acc{mlist[lane]};
         for (int w = 1; w < W; ++w) acc = warp_merge32(kmin(acc, KeyF{mlist[w * 32 + 31 - lane]}), lane);
         const float t = acc.shfl(K - 1).v;
-        if (lane == 0) reinterpret_cast<float *>(hdr)[2] = t;
+        if (lane == 0) {
+          reinterpret_cast<float *>(hdr)[2] = t;
+          hdr[1] = 0;  // a failed bound pass may have counted
+        }
       }
       __syncthreads();
       T = reinterpret_cast<const float *>(hdr)[2];
@@ -661,28 +715,10 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     const float theta = T + 2.f * p.band * am + fabsf(T) * 1e-6f;
 
     // ---- phase 3: collect every candidate the screen cannot exclude
-    int32_t *R = table + (H >> 1);
-    {
-      const int iters = (U + G - 1) / G;
-      for (int it = 0; it < iters; ++it) {
-        const int k = it * G + tid;
-        const float v = k < U ? scores[k] : 0.f;
-        const bool take = k < U && v <= theta;
-        const unsigned m = __ballot_sync(FULL, take);
-        if (m) {
-          const int leader = __ffs(m) - 1;
-          int b0 = 0;
-          if (lane == leader) b0 = atomicAdd(&hdr[1], __popc(m));
-          b0 = __shfl_sync(FULL, b0, leader);
-          if (take) {
-            const int r = b0 + __popc(m & lanemask_lt());
-            R[r] = list[k];
-            if (r < 32) rval[r] = v;
-          }
-        }
-      }
+    if (!collected) {
+      collect_r(scores, list, U, theta, R, rval, &hdr[1], tid, lane, G);
+      __syncthreads();
     }
-    __syncthreads();
     const int nR = hdr[1];
 
     // ---- phase 4: exact fp64 ranking of R, output (warp 0)
