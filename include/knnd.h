@@ -157,6 +157,25 @@ int knnd_random_kout(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint
                      uint64_t *consumed, int32_t *bad, int32_t *nbad, void *ws, size_t ws_bytes,
                      void *stream);
 
+/*
+ * Exact K nearest neighbours of a set of queries by brute force: row a holds
+ * the K smallest (fp64 score, id) over every point y != queries[a] —
+ * evaluation.py:83-90 (exact_knn's per-anchor body: s = batch_scores(x);
+ * s[x] = inf; _smallest_k(s, K), evaluation.py:53-71).  An fp32 screen of all
+ * n candidates keeps those within the rigorous error band of the K-th, which
+ * are rescored in fp64.  out_count[a] (device int32 per query) receives the
+ * number of candidates kept; a value > cap means row a was NOT written and
+ * must be recomputed with cap >= out_count[a].  out_scores (nullable) gets
+ * the fp64 scores.  flags: KNND_JOIN_NONPOS_LOG as for the local join.
+ * Workspace: knnd_exact_knn_workspace_bytes(nq, cap).  K in 1..64.
+ */
+size_t knnd_exact_knn_workspace_bytes(int64_t nq, int32_t cap);
+int knnd_exact_knn(const double *points, const float *log32, const double *log64,
+                   const double *xlogx, int64_t n, int32_t d, int32_t ld32,
+                   const int32_t *queries, int64_t nq, int32_t k, int32_t cap,
+                   int32_t *out_ids, double *out_scores, int32_t *out_count, void *ws,
+                   size_t ws_bytes, uint32_t flags, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -7,8 +7,9 @@ runs the same algorithm with the per-round local join, co-friend CSR,
 initial row sort and FCC statistic in hand-written sm_100a kernels
 (libknnd.so, C ABI in include/knnd.h).
 
-Only the KL ranking system is accelerated; other ranking systems, the
-metrizability checker, the exact oracle, the bench harness and the CLI are
+The exact K-NN ground truth and recall (evaluation.py:36-137) run on the GPU
+too (knnd_exact_knn).  Only the KL ranking system is accelerated; other
+ranking systems, the metrizability checker, the bench harness and the CLI are
 out of scope.
 """
 
@@ -34,6 +35,8 @@ from .descent import (
     run_round,
     run_to_fixed_point,
 )
+from . import evaluation
+from .evaluation import ExactKnnGraph, exact_knn, exact_rows, recall, sampled_recall, uniform_recall_sample
 from .similarity import KlRankingSystem, sample_simplex_uniform, validate_simplex_points
 
 __version__ = "0.1.0"
@@ -43,6 +46,7 @@ __all__ = [
     "Dataset",
     "DescentConfig",
     "EXPORTS",
+    "ExactKnnGraph",
     "ItemId",
     "KlRankingSystem",
     "KnndError",
@@ -55,6 +59,9 @@ __all__ = [
     "STREAM_RECALL",
     "ScoredRankingSystem",
     "derive_rng",
+    "evaluation",
+    "exact_knn",
+    "exact_rows",
     "fcc_samples",
     "friend_clustering_rate",
     "init_random_kout",
@@ -62,10 +69,13 @@ __all__ = [
     "load_library",
     "propose_new_friend_set",
     "random_kout_draws",
+    "recall",
     "round_budget",
     "run",
     "run_round",
     "run_to_fixed_point",
     "sample_simplex_uniform",
+    "sampled_recall",
+    "uniform_recall_sample",
     "validate_simplex_points",
 ]

@@ -20,7 +20,7 @@ INCLUDE = os.path.join(ROOT, "include")
 LIB_PATH = os.path.join(PKG_DIR, "libknnd.so")
 OBJ_DIR = os.path.join(PKG_DIR, "_obj")
 
-SOURCES = ["abi.cu", "prep.cu", "csr.cu", "join.cu", "rng.cu"]
+SOURCES = ["abi.cu", "prep.cu", "csr.cu", "join.cu", "rng.cu", "exact.cu"]
 HEADERS = ["common.cuh", "score.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
