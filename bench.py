@@ -49,6 +49,9 @@ CONFIGS = {
     "c4": (1_000_000, 50, 30),
     "c5": (10_000_000, 20, 20),
 }
+# recall@K of the reference's own final tables on uniform_recall_sample(n, 0, 10000)
+# (tests/golden/recall.json, recorded from the reference's runs)
+REF_RECALL = {"c1": 0.99382, "c2": 0.9738, "c3": 0.617925, "c4": 0.3055466666666667}
 CPU_SAMPLE_ANCHORS = 10_000_000  # i.e. every anchor of round 1 (bounded by n)
 
 
@@ -62,6 +65,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--no-recall", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
     return ap.parse_args()
 
@@ -226,12 +230,15 @@ def b200_arm(args):
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
     stream = torch.cuda.current_stream(dev)
 
+    last = {}
+
     def step(profile: bool):
         table = draws_dev.clone()
         eng.join_events = [] if profile else None
         state, hist = descend_resident(eng, tabs, table, smp_dev, cfg.fcc_sample_count, max_rounds)
         ev = eng.join_events or []
         eng.join_events = None
+        last["state"] = state
         return hist, ev
 
     for _ in range(args.warmup):
@@ -308,6 +315,20 @@ def b200_arm(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     e2e_value = e2e_comps / tt.item() if tt.item() > 0 else 0.0
 
+    # ---- recall@K of the final table (evaluation.py:111-137) on the reference's
+    # 10,000-id sample, exact rows by the GPU brute force; not timed
+    rec = None
+    if rank == 0 and not args.no_recall:
+        final = last["state"].friends
+        sample = b2.uniform_recall_sample(n, seed, 10_000)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = b2.sampled_recall(final, rs, sample, dev)
+        torch.cuda.synchronize()
+        rec = {"value": r, "sample": f"uniform_recall_sample(n, {seed}, 10000)",
+               "exact": "GPU brute force (knnd_exact_knn), fp64 (score, id) order",
+               "exact_s": time.perf_counter() - t0, "reference": REF_RECALL.get(args.config)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         tab, init, csr, sample = cpu_sample_setup(n, d, k, seed)
@@ -332,6 +353,7 @@ def b200_arm(args):
                     "time_to_termination_s": tt.item() / max(args.e2e_steps, 1)},
             "gpu_launches": launches_total,
             "roofline": roof,
+            "recall": rec,
             "cpu_baseline": cpu,
             "clocks": clk,
         }
