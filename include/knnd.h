@@ -176,6 +176,38 @@ int knnd_exact_knn(const double *points, const float *log32, const double *log64
                    int32_t *out_ids, double *out_scores, int32_t *out_count, void *ws,
                    size_t ws_bytes, uint32_t flags, void *stream);
 
+/*
+ * Squared-Euclidean scorer (EuclideanRankingSystem, similarity.py:119-140):
+ *   d2(x, y) = max(sq[x] + sq[y] - 2 * sum_j y_j x_j, 0),  sq = einsum("ij,ij->i").
+ * Tables (knnd_l2_prepare, from the fp64 vectors, their host-computed squared
+ * norms sq64 and a center mu, e.g. the column means):
+ *   rows64   (n, d+1) fp64  the vector, then sq
+ *   cand32   (n, ld32) fp32 [v - mu, |v - mu|^2, 0 ...]      ld32 >= d+1, % 4 == 0
+ *   anchor32 (n, ld32) fp32 [2 (v - mu), -1, 0 ...]
+ * The screen -sum anchor32[x] * cand32[y] equals d2(x, y) minus a per-anchor
+ * constant, so the same fused join / exact K-NN kernels run both metrics.
+ * maxnorm = max_y sqrt(sq[y]) bounds the fp64 rounding of d2 for the screen.
+ * Workspace of the L2 join: knnd_local_join_workspace_bytes(n, d + 1, ...).
+ */
+int knnd_l2_prepare(const double *vectors, const double *sq64, int64_t n, int32_t d, int32_t ld32,
+                    const double *center, float *cand32, float *anchor32, double *rows64, void *stream);
+int knnd_l2_batch_scores(const double *rows64, const double *sq64, int64_t n, int32_t d, int64_t x,
+                         const int32_t *ids, int64_t m, double *out, void *stream);
+int knnd_l2_sort_rows(const double *rows64, const double *sq64, int64_t n, int32_t d, int32_t k,
+                      int64_t row_lo, int64_t row_hi, const int32_t *draws, int32_t *out_ids,
+                      double *out_d2, void *stream);
+int knnd_l2_local_join(const float *anchor32, const float *cand32, const double *rows64,
+                       const double *sq64, int64_t n, int32_t d, int32_t ld32, double maxnorm,
+                       const int32_t *friends, int32_t k, const int64_t *indptr,
+                       const int32_t *indices, int64_t row_lo, int64_t row_hi, int32_t max_indeg,
+                       int32_t *out_ids, double *out_d2, int32_t *out_ucount,
+                       unsigned long long *tally, const float *bound_in, float *bound_out, void *ws,
+                       size_t ws_bytes, void *stream);
+int knnd_l2_exact_knn(const float *anchor32, const float *cand32, const double *rows64,
+                      const double *sq64, int64_t n, int32_t d, int32_t ld32, double maxnorm,
+                      const int32_t *queries, int64_t nq, int32_t k, int32_t cap, int32_t *out_ids,
+                      double *out_d2, int32_t *out_count, void *ws, size_t ws_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

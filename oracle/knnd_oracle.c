@@ -30,10 +30,18 @@
 #include <omp.h>
 #endif
 
-static double score(const double *pts, const double *lg, const double *xlogx, int d, int64_t x, int64_t y) {
+/* metric 0: KL (similarity.py:101-106), lg = log(points), xlogx = row entropies.
+ * metric 1: squared Euclidean (similarity.py:135-140), pts = lg = the vectors,
+ *           xlogx = their squared norms: max(sq[x] + sq[y] - 2 y.x, 0). */
+static double score(const double *pts, const double *lg, const double *xlogx, int d, int64_t x, int64_t y,
+                    int metric) {
   const double *px = pts + x * d, *ly = lg + y * d;
   double acc = 0.0;
   for (int j = 0; j < d; ++j) acc += ly[j] * px[j];
+  if (metric == 1) {
+    const double d2 = (xlogx[x] + xlogx[y]) - 2.0 * acc;
+    return d2 > 0.0 ? d2 : 0.0;
+  }
   return xlogx[x] - acc;
 }
 
@@ -85,9 +93,9 @@ static void scratch_fit(scratch_t *w, int64_t m) {
 }
 
 /* one anchor; returns |U|; writes the K best ids (and scores) */
-static int64_t join_one(const double *pts, const double *lg, const double *xlogx, int d, const int32_t *F, int k,
-                        const int64_t *indptr, const int32_t *indices, int64_t x, scratch_t *w, int32_t *row,
-                        double *row_s) {
+static int64_t join_one(const double *pts, const double *lg, const double *xlogx, int d, int metric,
+                        const int32_t *F, int k, const int64_t *indptr, const int32_t *indices, int64_t x,
+                        scratch_t *w, int32_t *row, double *row_s) {
   const int64_t c0 = indptr[x], c = indptr[x + 1] - c0;
   const int64_t pre = (k + c) * (int64_t)(k + 1);
   scratch_fit(w, pre);
@@ -117,7 +125,7 @@ static int64_t join_one(const double *pts, const double *lg, const double *xlogx
   int64_t bi[64];
   for (int64_t i = 0; i < u; ++i) {
     const int64_t y = w->ids[i];
-    const double s = score(pts, lg, xlogx, d, x, y);
+    const double s = score(pts, lg, xlogx, d, x, y, metric);
     if (nb == k && !key_lt(s, y, bs[k - 1], bi[k - 1])) continue;
     int p = nb < k ? nb++ : k - 1;
     while (p > 0 && key_lt(s, y, bs[p - 1], bi[p - 1])) {
@@ -140,9 +148,9 @@ static int64_t join_one(const double *pts, const double *lg, const double *xlogx
 }
 
 /* anchors[0..na) -> out rows i*k..; tally[0] += sum |U|, tally[1] += changed */
-int oracle_local_join(const double *pts, const double *lg, const double *xlogx, int64_t n, int d, const int32_t *F,
-                      int k, const int64_t *indptr, const int32_t *indices, const int64_t *anchors, int64_t na,
-                      int32_t *out, double *out_kl, int32_t *ucount, int64_t *tally, int nthreads) {
+int oracle_local_join(const double *pts, const double *lg, const double *xlogx, int64_t n, int d, int metric,
+                      const int32_t *F, int k, const int64_t *indptr, const int32_t *indices, const int64_t *anchors,
+                      int64_t na, int32_t *out, double *out_kl, int32_t *ucount, int64_t *tally, int nthreads) {
   (void)n;
   if (k < 1 || k > 64) return -1;
   int64_t comps = 0, changed = 0;
@@ -158,7 +166,8 @@ int oracle_local_join(const double *pts, const double *lg, const double *xlogx, 
     for (int64_t a = 0; a < na; ++a) {
       const int64_t x = anchors[a];
       int32_t *row = out + a * k;
-      int64_t u = join_one(pts, lg, xlogx, d, F, k, indptr, indices, x, &w, row, out_kl ? out_kl + a * k : 0);
+      int64_t u =
+          join_one(pts, lg, xlogx, d, metric, F, k, indptr, indices, x, &w, row, out_kl ? out_kl + a * k : 0);
       if (ucount) ucount[a] = (int32_t)u;
       comps += u;
       int diff = 0;
@@ -190,7 +199,7 @@ int32_t oracle_fcc(const int32_t *F, int64_t n, int k, const int64_t *xs, const 
 }
 
 /* stable sort of each row by score: insertion sort keyed (score, position) */
-void oracle_sort_rows(const double *pts, const double *lg, const double *xlogx, int64_t n, int d, int k,
+void oracle_sort_rows(const double *pts, const double *lg, const double *xlogx, int64_t n, int d, int metric, int k,
                       const int32_t *draws, int32_t *out, int nthreads) {
 #ifdef _OPENMP
   if (nthreads <= 0) nthreads = omp_get_max_threads();
@@ -201,7 +210,7 @@ void oracle_sort_rows(const double *pts, const double *lg, const double *xlogx, 
     int32_t id[64];
     for (int i = 0; i < k; ++i) {
       const int32_t y = draws[x * k + i];
-      const double v = score(pts, lg, xlogx, d, x, y);
+      const double v = score(pts, lg, xlogx, d, x, y, metric);
       int p = i;
       while (p > 0 && v < s[p - 1]) { /* strict: equal scores keep draw order */
         s[p] = s[p - 1];
@@ -216,7 +225,7 @@ void oracle_sort_rows(const double *pts, const double *lg, const double *xlogx, 
 }
 
 /* brute-force exact K-NN rows for the given queries (anchor excluded) */
-void oracle_exact_rows(const double *pts, const double *lg, const double *xlogx, int64_t n, int d, int k,
+void oracle_exact_rows(const double *pts, const double *lg, const double *xlogx, int64_t n, int d, int metric, int k,
                        const int64_t *queries, int64_t q, int32_t *out, int nthreads) {
 #ifdef _OPENMP
   if (nthreads <= 0) nthreads = omp_get_max_threads();
@@ -229,7 +238,7 @@ void oracle_exact_rows(const double *pts, const double *lg, const double *xlogx,
     int nb = 0;
     for (int64_t y = 0; y < n; ++y) {
       if (y == x) continue;
-      const double s = score(pts, lg, xlogx, d, x, y);
+      const double s = score(pts, lg, xlogx, d, x, y, metric);
       if (nb == k && !key_lt(s, y, bs[k - 1], bi[k - 1])) continue;
       int p = nb < k ? nb++ : k - 1;
       while (p > 0 && key_lt(s, y, bs[p - 1], bi[p - 1])) {

@@ -37,13 +37,13 @@ def lib():
         i64, i32 = C.c_int64, C.c_int
         L.oracle_transpose.argtypes = [P, i64, i32, P, P]
         L.oracle_transpose.restype = None
-        L.oracle_local_join.argtypes = [P, P, P, i64, i32, P, i32, P, P, P, i64, P, P, P, P, i32]
+        L.oracle_local_join.argtypes = [P, P, P, i64, i32, i32, P, i32, P, P, P, i64, P, P, P, P, i32]
         L.oracle_local_join.restype = i32
         L.oracle_fcc.argtypes = [P, i64, i32, P, P, P, i64]
         L.oracle_fcc.restype = C.c_int32
-        L.oracle_sort_rows.argtypes = [P, P, P, i64, i32, i32, P, P, i32]
+        L.oracle_sort_rows.argtypes = [P, P, P, i64, i32, i32, i32, P, P, i32]
         L.oracle_sort_rows.restype = None
-        L.oracle_exact_rows.argtypes = [P, P, P, i64, i32, i32, P, i64, P, i32]
+        L.oracle_exact_rows.argtypes = [P, P, P, i64, i32, i32, i32, P, i64, P, i32]
         L.oracle_exact_rows.restype = None
         _lib = L
     return _lib
@@ -60,10 +60,25 @@ def _c(a, dt):
 class Tables:
     """fp64 points, log and xlogx as similarity.py:91-93 computes them."""
 
+    metric = 0
+
     def __init__(self, points: np.ndarray):
         self.points = _c(points, np.float64)
         self.log = np.log(self.points)
         self.xlogx = np.einsum("ij,ij->i", self.points, self.log)
+        self.n, self.d = self.points.shape
+
+
+class L2Tables:
+    """Squared-Euclidean scoring (similarity.py:119-140): the vectors and their
+    squared norms (einsum, similarity.py:128) in the slots the C oracle reads."""
+
+    metric = 1
+
+    def __init__(self, vectors: np.ndarray):
+        self.points = _c(vectors, np.float64)
+        self.log = self.points
+        self.xlogx = np.einsum("ij,ij->i", self.points, self.points)
         self.n, self.d = self.points.shape
 
 
@@ -89,7 +104,7 @@ def local_join(tab: Tables, friends: np.ndarray, anchors: np.ndarray | None = No
     kl = np.empty((na, k), np.float64)
     uc = np.empty(na, np.int32)
     tally = np.zeros(2, np.int64)
-    rc = lib().oracle_local_join(_p(tab.points), _p(tab.log), _p(tab.xlogx), n, tab.d, _p(F), k, _p(ptr), _p(idx),
+    rc = lib().oracle_local_join(_p(tab.points), _p(tab.log), _p(tab.xlogx), n, tab.d, tab.metric, _p(F), k, _p(ptr), _p(idx),
                                  _p(anchors), na, _p(out), _p(kl), _p(uc), _p(tally), threads)
     if rc != 0:
         raise ValueError("oracle_local_join: unsupported K")
@@ -107,14 +122,14 @@ def sort_rows(tab: Tables, draws: np.ndarray, threads: int = 0) -> np.ndarray:
     D = _c(draws, np.int32)
     n, k = D.shape
     out = np.empty_like(D)
-    lib().oracle_sort_rows(_p(tab.points), _p(tab.log), _p(tab.xlogx), n, tab.d, k, _p(D), _p(out), threads)
+    lib().oracle_sort_rows(_p(tab.points), _p(tab.log), _p(tab.xlogx), n, tab.d, tab.metric, k, _p(D), _p(out), threads)
     return out
 
 
 def exact_rows(tab: Tables, queries: np.ndarray, k: int, threads: int = 0) -> np.ndarray:
     q = _c(queries, np.int64)
     out = np.empty((q.size, k), np.int32)
-    lib().oracle_exact_rows(_p(tab.points), _p(tab.log), _p(tab.xlogx), tab.n, tab.d, k, _p(q), q.size, _p(out),
+    lib().oracle_exact_rows(_p(tab.points), _p(tab.log), _p(tab.xlogx), tab.n, tab.d, tab.metric, k, _p(q), q.size, _p(out),
                             threads)
     return out
 

@@ -8,7 +8,8 @@ initial row sort and FCC statistic in hand-written sm_100a kernels
 (libknnd.so, C ABI in include/knnd.h).
 
 The exact K-NN ground truth and recall (evaluation.py:36-137) run on the GPU
-too (knnd_exact_knn).  Only the KL ranking system is accelerated; other
+too (knnd_exact_knn).  The KL and squared-Euclidean ranking systems
+(similarity.py:80-140) are accelerated through the same fused join; other
 ranking systems, the metrizability checker, the bench harness and the CLI are
 out of scope.
 """
@@ -37,7 +38,13 @@ from .descent import (
 )
 from . import evaluation
 from .evaluation import ExactKnnGraph, exact_knn, exact_rows, recall, sampled_recall, uniform_recall_sample
-from .similarity import KlRankingSystem, sample_simplex_uniform, validate_simplex_points
+from .similarity import (
+    EuclideanRankingSystem,
+    KlRankingSystem,
+    euclidean_ranking,
+    sample_simplex_uniform,
+    validate_simplex_points,
+)
 
 __version__ = "0.1.0"
 
@@ -46,6 +53,7 @@ __all__ = [
     "Dataset",
     "DescentConfig",
     "EXPORTS",
+    "EuclideanRankingSystem",
     "ExactKnnGraph",
     "ItemId",
     "KlRankingSystem",
@@ -59,6 +67,7 @@ __all__ = [
     "STREAM_RECALL",
     "ScoredRankingSystem",
     "derive_rng",
+    "euclidean_ranking",
     "evaluation",
     "exact_knn",
     "exact_rows",

@@ -39,6 +39,13 @@ struct ExactParams {
   int32_t *cand;   // nq x cap candidate ids
   int cap;
   int32_t *count;  // nq candidate counts (may exceed cap)
+  int32_t *out_ids;
+  double *out_scores;
+  int metric;      // score.cuh
+  int d64;         // fp64 row length (d, or d+1 for L2)
+  int pstride;     // row stride of `points`
+  const float *aside32;  // L2: anchor-side fp32 rows (null for KL)
+  double gamma, maxnorm;  // L2: absolute error scale of the fp64 values (join.cu exact_slack)
 };
 
 template <int NV4, int Q, bool ABS>
@@ -54,7 +61,13 @@ __global__ void __launch_bounds__(XWARPS * 32) exact_screen_kernel(ExactParams p
   for (int i = threadIdx.x; i < XQB * ld; i += blockDim.x) {
     const int r = i / ld, j = i % ld;
     float v = 0.f;
-    if (qb + r < p.nq && j < p.d) v = (float)p.points[(int64_t)p.queries[qb + r] * p.d + j];
+    if (qb + r < p.nq) {
+      const int64_t x = p.queries[qb + r];
+      if (p.aside32)
+        v = p.aside32[x * ld + j];
+      else if (j < p.d)
+        v = (float)p.points[x * p.pstride + j];
+    }
     xq[i] = v;
   }
   int qid[XQW];
@@ -215,7 +228,12 @@ __global__ void __launch_bounds__(XWARPS * 32) exact_screen_kernel(ExactParams p
           float a = am[qq];
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) a = fmaxf(a, __shfl_xor_sync(FULL, a, o));
-          th = T + 2.f * p.band * a + fabsf(T) * 1e-6f;
+          float slack = 0.f;
+          if (p.metric == METRIC_L2 && qid[qq] >= 0) {
+            const double r = sqrt(fmax(p.xlogx[qid[qq]], 0.0)) + p.maxnorm;
+            slack = (float)(p.gamma * r * r);
+          }
+          th = T + 2.f * (p.band * a + slack) + fabsf(T) * 1e-6f;
         }
         theta[qq] = qid[qq] >= 0 ? th : -__int_as_float(0x7f800000);  // padding queries take nothing
       }
@@ -240,7 +258,7 @@ __global__ void exact_rank_kernel(ExactParams p, int32_t *__restrict__ out_ids, 
     if (nc > p.cap) continue;  // overflow: the caller reruns this query
     const int x = p.queries[a];
     __syncwarp();
-    for (int j = lane; j < p.d; j += 32) x64[j] = p.points[(int64_t)x * p.d + j];
+    for (int j = lane; j < p.d; j += 32) x64[j] = p.points[(int64_t)x * p.pstride + j];
     __syncwarp();
     const double xl = p.xlogx[x];
     WarpTopK<KeyD, KPL> top;
@@ -250,7 +268,7 @@ __global__ void exact_rank_kernel(ExactParams p, int32_t *__restrict__ out_ids, 
       KeyD k = KeyD::inf();
       if (b + lane < nc) {
         const int y = c[b + lane];
-        k = {exact_score(x64, p.log64 + (int64_t)y * p.d, p.d, xl), y};
+        k = {exact_score_m(x64, p.log64 + (int64_t)y * p.d64, p.d, xl, p.metric), y};
       }
       if (b == 0)
         top.first(k, lane);
@@ -311,43 +329,29 @@ size_t knnd_exact_knn_workspace_bytes(int64_t nq, int32_t cap) {
   return align_up((size_t)nq * (size_t)cap * 4, 256) + 256;
 }
 
-int knnd_exact_knn(const double *points, const float *log32, const double *log64, const double *xlogx, int64_t n,
-                   int32_t d, int32_t ld32, const int32_t *queries, int64_t nq, int32_t k, int32_t cap,
-                   int32_t *out_ids, double *out_scores, int32_t *out_count, void *ws, size_t ws_bytes,
-                   uint32_t flags, void *stream) {
-  KNND_CHECK_ARG(points && log32 && log64 && xlogx && out_count && (nq == 0 || (queries && out_ids)),
-                 "knnd_exact_knn: null pointer");
-  KNND_CHECK_ARG(n >= 2 && d >= 1, "knnd_exact_knn: bad shape n=%lld d=%d", (long long)n, d);
-  KNND_CHECK_ARG(ld32 >= d && ld32 % 4 == 0, "knnd_exact_knn: ld32=%d must be >= d and a multiple of 4", ld32);
-  KNND_CHECK_ARG(n < ((int64_t)1 << 31), "knnd_exact_knn: n must be < 2^31");
-  KNND_CHECK_ARG(cap >= 1 && nq >= 0, "knnd_exact_knn: bad cap %d / nq %lld", cap, (long long)nq);
+static int exact_run(const char *who, ExactParams &p, int32_t dplan, int32_t k, void *ws, size_t ws_bytes,
+                     void *stream) {
+  const int64_t n = p.n, nq = p.nq;
+  const int32_t d = p.d, ld32 = p.ld, cap = p.cap;
+  KNND_CHECK_ARG(p.count && (nq == 0 || (p.queries && p.out_ids)), "%s: null pointer", who);
+  KNND_CHECK_ARG(n >= 2 && d >= 1, "%s: bad shape n=%lld d=%d", who, (long long)n, d);
+  KNND_CHECK_ARG(ld32 >= dplan && ld32 % 4 == 0, "%s: ld32=%d must be >= %d and a multiple of 4", who, ld32, dplan);
+  KNND_CHECK_ARG(n < ((int64_t)1 << 31), "%s: n must be < 2^31", who);
+  KNND_CHECK_ARG(cap >= 1 && nq >= 0, "%s: bad cap %d / nq %lld", who, cap, (long long)nq);
   if (k < 1 || k > 64 || k >= n) {
-    set_error("knnd_exact_knn: K=%d unsupported (1..64, < n)", k);
+    set_error("%s: K=%d unsupported (1..64, < n)", who, k);
     return KNND_EUNSUPPORTED;
   }
   if (nq == 0) return KNND_OK;
   const size_t need = knnd_exact_knn_workspace_bytes(nq, cap);
   if (!ws || ws_bytes < need) {
-    set_error("knnd_exact_knn: workspace %zu < %zu bytes", ws_bytes, need);
+    set_error("%s: workspace %zu < %zu bytes", who, ws_bytes, need);
     return KNND_EWORKSPACE;
   }
   cudaStream_t st = as_stream(stream);
-  ExactParams p;
-  p.points = points;
-  p.log32 = log32;
-  p.log64 = log64;
-  p.xlogx = xlogx;
-  p.n = n;
-  p.d = d;
-  p.ld = ld32;
   p.K = k;
-  p.queries = queries;
-  p.nq = nq;
   p.band = (float)((ld32 + 8) * 0x1p-24);
-  p.nonpos = (flags & KNND_JOIN_NONPOS_LOG) ? 1 : 0;
   p.cand = static_cast<int32_t *>(ws);
-  p.cap = cap;
-  p.count = out_count;
   const int rc = k <= 32 ? dispatch_screen<2>(p, st) : dispatch_screen<4>(p, st);
   if (rc) return rc;
   const int wpb = 8;
@@ -355,11 +359,66 @@ int knnd_exact_knn(const double *points, const float *log32, const double *log64
   if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
   const size_t smem = (size_t)wpb * d * sizeof(double);
   if (k <= 32)
-    exact_rank_kernel<1><<<(unsigned)blocks, wpb * 32, smem, st>>>(p, out_ids, out_scores);
+    exact_rank_kernel<1><<<(unsigned)blocks, wpb * 32, smem, st>>>(p, p.out_ids, p.out_scores);
   else
-    exact_rank_kernel<2><<<(unsigned)blocks, wpb * 32, smem, st>>>(p, out_ids, out_scores);
+    exact_rank_kernel<2><<<(unsigned)blocks, wpb * 32, smem, st>>>(p, p.out_ids, p.out_scores);
   KNND_LAUNCHED(1);
   return KNND_OK;
+}
+
+int knnd_exact_knn(const double *points, const float *log32, const double *log64, const double *xlogx, int64_t n,
+                   int32_t d, int32_t ld32, const int32_t *queries, int64_t nq, int32_t k, int32_t cap,
+                   int32_t *out_ids, double *out_scores, int32_t *out_count, void *ws, size_t ws_bytes,
+                   uint32_t flags, void *stream) {
+  KNND_CHECK_ARG(points && log32 && log64 && xlogx, "knnd_exact_knn: null pointer");
+  ExactParams p{};
+  p.points = points;
+  p.log32 = log32;
+  p.log64 = log64;
+  p.xlogx = xlogx;
+  p.n = n;
+  p.d = d;
+  p.ld = ld32;
+  p.queries = queries;
+  p.nq = nq;
+  p.nonpos = (flags & KNND_JOIN_NONPOS_LOG) ? 1 : 0;
+  p.cap = cap;
+  p.count = out_count;
+  p.out_ids = out_ids;
+  p.out_scores = out_scores;
+  p.metric = METRIC_KL;
+  p.d64 = d;
+  p.pstride = d;
+  return exact_run("knnd_exact_knn", p, d, k, ws, ws_bytes, stream);
+}
+
+int knnd_l2_exact_knn(const float *anchor32, const float *cand32, const double *rows64, const double *sq64,
+                      int64_t n, int32_t d, int32_t ld32, double maxnorm, const int32_t *queries, int64_t nq,
+                      int32_t k, int32_t cap, int32_t *out_ids, double *out_d2, int32_t *out_count, void *ws,
+                      size_t ws_bytes, void *stream) {
+  KNND_CHECK_ARG(anchor32 && cand32 && rows64 && sq64, "knnd_l2_exact_knn: null pointer");
+  ExactParams p{};
+  p.points = rows64;
+  p.log32 = cand32;
+  p.log64 = rows64;
+  p.xlogx = sq64;
+  p.n = n;
+  p.d = d;
+  p.ld = ld32;
+  p.queries = queries;
+  p.nq = nq;
+  p.nonpos = 0;
+  p.cap = cap;
+  p.count = out_count;
+  p.out_ids = out_ids;
+  p.out_scores = out_d2;
+  p.metric = METRIC_L2;
+  p.d64 = d + 1;
+  p.pstride = d + 1;
+  p.aside32 = anchor32;
+  p.gamma = (d + 4) * 0x1p-53;
+  p.maxnorm = maxnorm;
+  return exact_run("knnd_l2_exact_knn", p, d + 1, k, ws, ws_bytes, stream);
 }
 
 }  // extern "C"

@@ -59,7 +59,22 @@ struct JoinParams {
   int nonpos;  // every log coordinate <= 0: sum |x log y| == -sum x log y exactly
   const float *__restrict__ bound_in;  // per own row: max screened value of the current row (or NaN)
   float *__restrict__ bound_out;       // the same for the row written this round
+  // metric (score.cuh): KL, or squared Euclidean (EuclideanRankingSystem, similarity.py:119-140)
+  int metric;
+  int d64;                               // fp64 row length of log64 (d; d+1 for L2: the vector, then |v|^2)
+  int pstride;                           // row stride of `points` (the anchor's fp64 coordinates)
+  const float *__restrict__ aside32;     // L2: anchor-side fp32 rows (2(x-mu), -1); KL: null (from points)
+  double gamma;                          // L2: |our fp64 d2 - true d2| <= gamma (|x| + maxnorm)^2
+  double maxnorm;
 };
+
+// absolute slack of the exact fp64 values (0 for KL, whose error is relative
+// and inside p.band); the screen band of an anchor is 2 (band*am + slack)
+__device__ __forceinline__ float exact_slack(const JoinParams &p, double xl) {
+  if (p.metric != METRIC_L2) return 0.f;
+  const double r = sqrt(fmax(xl, 0.0)) + p.maxnorm;
+  return (float)(p.gamma * r * r);
+}
 
 __host__ __device__ inline size_t al16(size_t v) { return (v + 15) & ~(size_t)15; }
 
@@ -180,10 +195,10 @@ __device__ __forceinline__ void screen_row(const float *row, const float *x32, i
     a = fmaf(-xv.y, l.y, a);
     a = fmaf(-xv.z, l.z, a);
     a = fmaf(-xv.w, l.w, a);
-    b = fmaf(xv.x, fabsf(l.x), b);
-    b = fmaf(xv.y, fabsf(l.y), b);
-    b = fmaf(xv.z, fabsf(l.z), b);
-    b = fmaf(xv.w, fabsf(l.w), b);
+    b = fmaf(fabsf(xv.x), fabsf(l.x), b);
+    b = fmaf(fabsf(xv.y), fabsf(l.y), b);
+    b = fmaf(fabsf(xv.z), fabsf(l.z), b);
+    b = fmaf(fabsf(xv.w), fabsf(l.w), b);
   }
   ce = a;
   ab = b;
@@ -218,10 +233,10 @@ __device__ __forceinline__ void screen_row_reg(const float *row, const float4 (&
     a = fmaf(-xr[q].y, l.y, a);
     a = fmaf(-xr[q].z, l.z, a);
     a = fmaf(-xr[q].w, l.w, a);
-    b = fmaf(xr[q].x, fabsf(l.x), b);
-    b = fmaf(xr[q].y, fabsf(l.y), b);
-    b = fmaf(xr[q].z, fabsf(l.z), b);
-    b = fmaf(xr[q].w, fabsf(l.w), b);
+    b = fmaf(fabsf(xr[q].x), fabsf(l.x), b);
+    b = fmaf(fabsf(xr[q].y), fabsf(l.y), b);
+    b = fmaf(fabsf(xr[q].z), fabsf(l.z), b);
+    b = fmaf(fabsf(xr[q].w), fabsf(l.w), b);
   }
   ce = a;
   ab = b;
@@ -246,10 +261,10 @@ __device__ __forceinline__ void stage_rows_f64(double *stage, int sd, const doub
 }
 
 // exact fp64 score from a staged row: same left-to-right FMA order as exact_score
-__device__ __forceinline__ double exact_from_row(const double *row, const double *x64, int d, double xl) {
+__device__ __forceinline__ double exact_from_row(const double *row, const double *x64, int d, double xl, int metric) {
   double acc = 0.0;
   for (int j = 0; j < d; ++j) acc = fma(x64[j], row[j], acc);
-  return xl - acc;
+  return finish_score(metric, xl, metric == METRIC_L2 ? row[d] : 0.0, acc);
 }
 
 // emit the sorted row (lanes hold the exact top-K), return the change flag
@@ -275,7 +290,7 @@ __device__ __forceinline__ bool emit_row(const JoinParams &p, const WarpTopK<Key
 template <int KPL>
 __device__ __forceinline__ void exact_rank(const JoinParams &p, WarpTopK<KeyD, KPL> &ex, const int32_t *ids, int nR,
                                            double *stage64, int rcap, const double *x64, double xl, int lane) {
-  const int d = p.d, sd = d | 1;
+  const int d = p.d64, sd = d | 1;
   ex.init();
   for (int b = 0; b < nR; b += rcap) {
     const int nrow = min(rcap, nR - b);
@@ -299,7 +314,7 @@ __device__ __forceinline__ void exact_rank(const JoinParams &p, WarpTopK<KeyD, K
     __syncwarp();
     KeyD key = KeyD::inf();
     if (lane < nrow) {
-      key.s = exact_from_row(stage64 + lane * sd, x64, d, xl);
+      key.s = exact_from_row(stage64 + lane * sd, x64, p.d, xl, p.metric);
       key.id = ids[b + lane];
     }
     __syncwarp();
@@ -316,14 +331,13 @@ __device__ __forceinline__ void exact_rank(const JoinParams &p, WarpTopK<KeyD, K
 // top K+1 — hence the row — is the screened order (exact ties are impossible
 // at that distance).  Returns false (nothing written) when a gap is too small.
 __device__ __forceinline__ bool certify_row(const JoinParams &p, const int32_t *ids, const float *vals, int nR,
-                                            float am, int x, int64_t xr, int lane, bool &diff, float &kth) {
+                                            float band, int x, int64_t xr, int lane, bool &diff, float &kth) {
   const int K = p.K;
   KeyU key = KeyU::inf();
   if (lane < nR) key = KeyU::make(vals[lane], ids[lane]);
   key = warp_sort32(key, lane);
   const float kv = key.v();
   const float nextv = __shfl_down_sync(FULL, kv, 1);
-  const float band = 2.f * p.band * am;
   const float gap_need = band + fabsf(kv) * 2e-6f + 1e-30f;
   const bool need_check = lane < K && lane + 1 < nR;  // nR == K: the set is R itself
   const bool ok = !need_check || (nextv - kv > gap_need);
@@ -475,7 +489,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     wrows = 0;  // set per anchor (the staging area follows the scores)
     wstage = nullptr;
     stage64 = reinterpret_cast<double *>(table);  // lower half, free in phase 4
-    rcap64 = min(32, (2 * H) / ((p.d | 1) * 8));
+    rcap64 = min(32, (2 * H) / ((p.d64 | 1) * 8));
   }
   const int K = p.K, K1 = K + 1;
   const int d = p.d, ld = p.ld;
@@ -504,8 +518,10 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     }
     for (int i = tid; i < 2 * NBIN; i += G) hist[i] = 0;
     for (int i = tid; i < nS; i += G) S[i] = i < K ? __ldg(p.F + (int64_t)x * K + i) : __ldg(p.indices + c0 + (i - K));
-    for (int i = tid; i < ld; i += G) x32[i] = i < d ? (float)__ldg(p.points + (int64_t)x * d + i) : 0.f;
-    for (int i = tid; i < d; i += G) x64[i] = __ldg(p.points + (int64_t)x * d + i);
+    for (int i = tid; i < ld; i += G)
+      x32[i] = p.aside32 ? __ldg(p.aside32 + (int64_t)x * ld + i)
+                         : (i < d ? (float)__ldg(p.points + (int64_t)x * p.pstride + i) : 0.f);
+    for (int i = tid; i < d; i += G) x64[i] = __ldg(p.points + (int64_t)x * p.pstride + i);
     if (tid == 0) {
       hdr[0] = 0;
       hdr[1] = 0;
@@ -556,6 +572,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
       wstage = reinterpret_cast<float *>(table + u4) + (size_t)warp * per_warp_floats;
     }
     float mn = __int_as_float(0x7f800000), mx = -mn, am = 0.f;
+    const float slack = exact_slack(p, __ldg(p.xlogx + x));
     float best0 = mn, best1 = mn;  // this lane's two smallest screened values
     float4 xreg[NV4 > 0 ? NV4 : 1];  // the anchor's fp32 row in registers
     if constexpr (NV4 > 0) {
@@ -629,7 +646,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
         float ab = 0.f;
 #pragma unroll
         for (int w = 0; w < W; ++w) ab = fmaxf(ab, red[w * 4 + 2]);
-        const float th0 = T0 + 2.f * p.band * ab + fabsf(T0) * 1e-6f;
+        const float th0 = T0 + 2.f * (p.band * ab + slack) + fabsf(T0) * 1e-6f;
         collect_r(scores, list, U, th0, R, rval, &hdr[1], tid, lane, G);
         __syncthreads();
         if (hdr[1] <= 32) {
@@ -712,7 +729,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
         T += (fabsf(T) + range) * 1e-6f;  // covers the rounding of t and of this line
       }
     }
-    const float theta = T + 2.f * p.band * am + fabsf(T) * 1e-6f;
+    const float theta = T + 2.f * (p.band * am + slack) + fabsf(T) * 1e-6f;
 
     // ---- phase 3: collect every candidate the screen cannot exclude
     if (!collected) {
@@ -725,7 +742,8 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     if (warp == 0) {
       bool diff;
       float kth = theta;  // every member of the new row has a screened value <= theta
-      if (!(KPL == 1 && p.out_kl == nullptr && nR <= 32 && certify_row(p, R, rval, nR, am, x, xr, lane, diff, kth))) {
+      if (!(KPL == 1 && p.out_kl == nullptr && nR <= 32 &&
+            certify_row(p, R, rval, nR, 2.f * (p.band * am + slack), x, xr, lane, diff, kth))) {
         WarpTopK<KeyD, KPL> ex;
         exact_rank<KPL>(p, ex, R, nR, stage64, rcap64, x64, __ldg(p.xlogx + x), lane);
         diff = emit_row<KPL>(p, ex, x, xr, lane);
@@ -799,7 +817,7 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
   float *scores = reinterpret_cast<float *>(table);            // phase 2-3: [0, U)
   double *stage64 = reinterpret_cast<double *>(table);         // phase 4: whole table
   const int K = p.K, K1 = K + 1;
-  const int d = p.d, ld = p.ld, sd = d | 1;
+  const int d = p.d, ld = p.ld, sd = p.d64 | 1;
   const int rcap64 = min(32, (4 * H) / (sd * 8));
   const int Gq = 32 / K1, Gr = 32 % K1;
   const int s_init = lane / K1, j_init = lane % K1;
@@ -831,8 +849,10 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
       for (int i = lane; i < (H >> 2); i += 32) t4[i] = make_int4(EMPTY, EMPTY, EMPTY, EMPTY);
     }
     for (int i = lane; i < nS; i += 32) S[i] = i < K ? __ldg(p.F + (int64_t)x * K + i) : __ldg(p.indices + c0 + (i - K));
-    for (int i = lane; i < ld; i += 32) x32[i] = i < d ? (float)__ldg(p.points + (int64_t)x * d + i) : 0.f;
-    for (int i = lane; i < d; i += 32) x64[i] = __ldg(p.points + (int64_t)x * d + i);
+    for (int i = lane; i < ld; i += 32)
+      x32[i] = p.aside32 ? __ldg(p.aside32 + (int64_t)x * ld + i)
+                         : (i < d ? (float)__ldg(p.points + (int64_t)x * p.pstride + i) : 0.f);
+    for (int i = lane; i < d; i += 32) x64[i] = __ldg(p.points + (int64_t)x * p.pstride + i);
     __syncwarp();
     float4 xreg[NV4 > 0 ? NV4 : 1];  // the anchor's fp32 row in registers
     if constexpr (NV4 > 0) {
@@ -896,6 +916,7 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
 #pragma unroll
     for (int q = 0; q < Q; ++q) best[q] = __int_as_float(0x7f800000);
     float am = 0.f;
+    const float slack = exact_slack(p, __ldg(p.xlogx + x));
     // ids of batch b+1 are in a register while batch b computes; batch b+2's are being loaded
     // two staging buffers in the table past the scores ([0, U), U <= H/2)
     const int u4 = (U + 3) & ~3;
@@ -980,7 +1001,7 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
     const float T0 = p.bound_in ? p.bound_in[xr] : __int_as_float(0x7fc00000);
     float T;
     if (KPL == 1 && isfinite(T0)) {
-      const float th0 = T0 + 2.f * p.band * am + fabsf(T0) * 1e-6f;
+      const float th0 = T0 + 2.f * (p.band * am + slack) + fabsf(T0) * 1e-6f;
       int cnt = 0;
       for (int k0 = 0; k0 < U; k0 += 32) {
         const int k = k0 + lane;
@@ -990,7 +1011,7 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
     } else {
       T = lane_pair_T();
     }
-    const float theta = T + 2.f * p.band * am + fabsf(T) * 1e-6f;
+    const float theta = T + 2.f * (p.band * am + slack) + fabsf(T) * 1e-6f;
 
     // ---- phase 3: R (ids and screened values) in place at the front of list / scores
     int nR = 0;
@@ -1013,7 +1034,7 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
     bool diff;
     float kth = theta;  // every member of the new row has a screened value <= theta
     if (!(KPL == 1 && p.out_kl == nullptr && nR <= 32 &&
-          certify_row(p, list, scores, nR, am, x, xr, lane, diff, kth))) {
+          certify_row(p, list, scores, nR, 2.f * (p.band * am + slack), x, xr, lane, diff, kth))) {
       WarpTopK<KeyD, KPL> ex;
       exact_rank<KPL>(p, ex, list, nR, stage64, rcap64, x64, __ldg(p.xlogx + x), lane);
       diff = emit_row<KPL>(p, ex, x, xr, lane);
@@ -1314,31 +1335,32 @@ size_t knnd_local_join_workspace_bytes(int64_t n, int32_t d, int32_t k, int64_t 
   return make_plan(row_hi - row_lo, d, k, max_indeg).total;
 }
 
-int knnd_local_join(const double *points, const float *log32, const double *log64, const double *xlogx, int64_t n,
-                    int32_t d, int32_t ld32, const int32_t *friends, int32_t k, const int64_t *indptr,
-                    const int32_t *indices, int64_t row_lo, int64_t row_hi, int32_t max_indeg, int32_t *out_ids,
-                    double *out_kl, int32_t *out_ucount, unsigned long long *tally, const float *bound_in,
-                    float *bound_out, void *ws, size_t ws_bytes, uint32_t flags, void *stream) {
-  KNND_CHECK_ARG(points && log32 && log64 && xlogx && friends && indptr && indices && out_ids && tally,
-                 "knnd_local_join: null pointer");
-  KNND_CHECK_ARG(n >= 2 && d >= 1, "knnd_local_join: bad shape n=%lld d=%d", (long long)n, d);
-  KNND_CHECK_ARG(ld32 >= d && ld32 % 4 == 0, "knnd_local_join: ld32=%d must be >= d and a multiple of 4", ld32);
-  KNND_CHECK_ARG(0 <= row_lo && row_lo <= row_hi && row_hi <= n, "knnd_local_join: bad row range");
-  KNND_CHECK_ARG(n * (int64_t)k < ((int64_t)1 << 31), "knnd_local_join: n*K must be < 2^31");
-  KNND_CHECK_ARG(max_indeg >= 0 && max_indeg <= n, "knnd_local_join: bad max_indeg %d", max_indeg);
+}  // extern "C"
+
+// shared by the KL and L2 entries: validation that does not depend on the
+// metric, the plan, and the class launches
+static int join_run(const char *who, JoinParams &p, int64_t n, int32_t dplan, int32_t k, int64_t row_lo,
+                    int64_t row_hi, int32_t max_indeg, void *ws, size_t ws_bytes, void *stream) {
+  const int32_t d = p.d, ld32 = p.ld;
+  KNND_CHECK_ARG(p.F && p.indptr && p.indices && p.out_ids && p.tally, "%s: null pointer", who);
+  KNND_CHECK_ARG(n >= 2 && d >= 1, "%s: bad shape n=%lld d=%d", who, (long long)n, d);
+  KNND_CHECK_ARG(ld32 >= dplan && ld32 % 4 == 0, "%s: ld32=%d must be >= %d and a multiple of 4", who, ld32, dplan);
+  KNND_CHECK_ARG(0 <= row_lo && row_lo <= row_hi && row_hi <= n, "%s: bad row range", who);
+  KNND_CHECK_ARG(n * (int64_t)k < ((int64_t)1 << 31), "%s: n*K must be < 2^31", who);
+  KNND_CHECK_ARG(max_indeg >= 0 && max_indeg <= n, "%s: bad max_indeg %d", who, max_indeg);
   if (k < 2 || k > 64) {
-    set_error("knnd_local_join: K=%d unsupported (2..64)", k);
+    set_error("%s: K=%d unsupported (2..64)", who, k);
     return KNND_EUNSUPPORTED;
   }
   const int64_t m = row_hi - row_lo;
   if (m == 0) return KNND_OK;
   if (((int64_t)k + max_indeg) * (k + 1) > ((int64_t)1 << 29)) {
-    set_error("knnd_local_join: pre-dedup bound (K+%d)(K+1) too large", max_indeg);
+    set_error("%s: pre-dedup bound (K+%d)(K+1) too large", who, max_indeg);
     return KNND_EUNSUPPORTED;
   }
-  const Plan P = make_plan(m, d, k, max_indeg);
+  const Plan P = make_plan(m, dplan, k, max_indeg);
   if (ws_bytes < P.total || !ws) {
-    set_error("knnd_local_join: workspace %zu < %zu bytes", ws_bytes, P.total);
+    set_error("%s: workspace %zu < %zu bytes", who, ws_bytes, P.total);
     return KNND_EWORKSPACE;
   }
   cudaStream_t st = as_stream(stream);
@@ -1347,28 +1369,12 @@ int knnd_local_join(const double *points, const float *log32, const double *log6
   int32_t *counts = reinterpret_cast<int32_t *>(w + P.counts_off);
   int32_t *slabs = reinterpret_cast<int32_t *>(w + P.slab_off);
   int32_t *glists = reinterpret_cast<int32_t *>(w + P.glist_off);
-
-  JoinParams p;
-  p.points = points;
-  p.log32 = log32;
-  p.log64 = log64;
-  p.xlogx = xlogx;
-  p.F = friends;
-  p.indptr = indptr;
-  p.indices = indices;
-  p.out_ids = out_ids;
-  p.out_kl = out_kl;
-  p.out_ucount = out_ucount;
-  p.tally = tally;
+  const int64_t *indptr = p.indptr;
+  unsigned long long *tally = p.tally;
   p.lo = row_lo;
-  p.d = d;
-  p.ld = ld32;
   p.K = k;
   // rigorous bound on |fp32 screen - fp64| relative to sum |x*log y| (+ margin)
   p.band = (float)((ld32 + 8) * 0x1p-24);
-  p.nonpos = (flags & KNND_JOIN_NONPOS_LOG) ? 1 : 0;
-  p.bound_in = bound_in;
-  p.bound_out = bound_out;
 
   KNND_CUDA(cudaMemsetAsync(counts, 0, 64, st));
   {
@@ -1414,6 +1420,71 @@ int knnd_local_join(const double *points, const float *log32, const double *log6
     }
   }
   return KNND_OK;
+}
+
+extern "C" {
+
+int knnd_local_join(const double *points, const float *log32, const double *log64, const double *xlogx, int64_t n,
+                    int32_t d, int32_t ld32, const int32_t *friends, int32_t k, const int64_t *indptr,
+                    const int32_t *indices, int64_t row_lo, int64_t row_hi, int32_t max_indeg, int32_t *out_ids,
+                    double *out_kl, int32_t *out_ucount, unsigned long long *tally, const float *bound_in,
+                    float *bound_out, void *ws, size_t ws_bytes, uint32_t flags, void *stream) {
+  KNND_CHECK_ARG(points && log32 && log64 && xlogx, "knnd_local_join: null pointer");
+  JoinParams p{};
+  p.points = points;
+  p.log32 = log32;
+  p.log64 = log64;
+  p.xlogx = xlogx;
+  p.F = friends;
+  p.indptr = indptr;
+  p.indices = indices;
+  p.out_ids = out_ids;
+  p.out_kl = out_kl;
+  p.out_ucount = out_ucount;
+  p.tally = tally;
+  p.d = d;
+  p.ld = ld32;
+  p.nonpos = (flags & KNND_JOIN_NONPOS_LOG) ? 1 : 0;
+  p.bound_in = bound_in;
+  p.bound_out = bound_out;
+  p.metric = METRIC_KL;
+  p.d64 = d;
+  p.pstride = d;
+  p.aside32 = nullptr;
+  return join_run("knnd_local_join", p, n, d, k, row_lo, row_hi, max_indeg, ws, ws_bytes, stream);
+}
+
+int knnd_l2_local_join(const float *anchor32, const float *cand32, const double *rows64, const double *sq64,
+                       int64_t n, int32_t d, int32_t ld32, double maxnorm, const int32_t *friends, int32_t k,
+                       const int64_t *indptr, const int32_t *indices, int64_t row_lo, int64_t row_hi,
+                       int32_t max_indeg, int32_t *out_ids, double *out_d2, int32_t *out_ucount,
+                       unsigned long long *tally, const float *bound_in, float *bound_out, void *ws, size_t ws_bytes,
+                       void *stream) {
+  KNND_CHECK_ARG(anchor32 && cand32 && rows64 && sq64, "knnd_l2_local_join: null pointer");
+  JoinParams p{};
+  p.points = rows64;  // the anchor's fp64 coordinates: the first d entries of its row
+  p.log32 = cand32;
+  p.log64 = rows64;
+  p.xlogx = sq64;
+  p.F = friends;
+  p.indptr = indptr;
+  p.indices = indices;
+  p.out_ids = out_ids;
+  p.out_kl = out_d2;
+  p.out_ucount = out_ucount;
+  p.tally = tally;
+  p.d = d;
+  p.ld = ld32;
+  p.nonpos = 0;
+  p.bound_in = bound_in;
+  p.bound_out = bound_out;
+  p.metric = METRIC_L2;
+  p.d64 = d + 1;
+  p.pstride = d + 1;
+  p.aside32 = anchor32;
+  p.gamma = (d + 4) * 0x1p-53;
+  p.maxnorm = maxnorm;
+  return join_run("knnd_l2_local_join", p, n, d + 1, k, row_lo, row_hi, max_indeg, ws, ws_bytes, stream);
 }
 
 }  // extern "C"

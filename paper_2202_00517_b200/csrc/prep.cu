@@ -33,25 +33,63 @@ __global__ void kl_prepare_kernel(const double *__restrict__ pts, int64_t n, int
 }
 
 // core.py:97-103 / similarity.py:101-106 — exact scores of ids against anchor x
-__global__ void batch_scores_kernel(const double *__restrict__ pts, const double *__restrict__ log64,
-                                    const double *__restrict__ xlogx, int d, int64_t x,
+// (L2: similarity.py:135-140, pts = log64 = the vector rows with |v|^2 appended)
+__global__ void batch_scores_kernel(const double *__restrict__ pts, int pstride, const double *__restrict__ log64,
+                                    int d64, const double *__restrict__ xlogx, int d, int metric, int64_t x,
                                     const int32_t *__restrict__ ids, int64_t m, double *__restrict__ out) {
   extern __shared__ double xs[];
-  for (int j = threadIdx.x; j < d; j += blockDim.x) xs[j] = pts[x * d + j];
+  for (int j = threadIdx.x; j < d; j += blockDim.x) xs[j] = pts[x * pstride + j];
   __syncthreads();
   const double xl = xlogx[x];
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
     int y = ids[i];
-    out[i] = exact_score(xs, log64 + (int64_t)y * d, d, xl);
+    out[i] = exact_score_m(xs, log64 + (int64_t)y * d64, d, xl, metric);
+  }
+}
+
+// similarity.py:126-128 + the L2 screen tables: rows64 = [v, |v|^2] (the squared
+// norm computed by the caller with numpy's einsum, as the reference does),
+// cand32 = [v - mu, |v - mu|^2, 0...], anchor32 = [2 (v - mu), -1, 0...]: the
+// screen's -sum anchor32 * cand32 = |y - mu|^2 - 2 (x - mu).(y - mu) is d2(x, y)
+// minus a per-anchor constant.  One warp per row.
+__global__ void l2_prepare_kernel(const double *__restrict__ vecs, const double *__restrict__ sq, int64_t n, int d,
+                                  int ld, const double *__restrict__ center, float *__restrict__ cand32,
+                                  float *__restrict__ anchor32, double *__restrict__ rows64) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
+    double part = 0.0;
+    for (int j = lane; j < ld; j += 32) {
+      float c32 = 0.f, a32 = 0.f;
+      if (j < d) {
+        const double v = vecs[r * d + j];
+        const double c = v - center[j];
+        rows64[r * (d + 1) + j] = v;
+        c32 = (float)c;
+        a32 = (float)(2.0 * c);
+        part = fma(c, c, part);
+      }
+      if (j != d) {
+        cand32[r * ld + j] = c32;
+        anchor32[r * ld + j] = a32;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(FULL, part, o);
+    if (lane == 0) {
+      cand32[r * ld + d] = (float)part;
+      anchor32[r * ld + d] = -1.f;
+      rows64[r * (d + 1) + d] = sq[r];
+    }
   }
 }
 
 // descent.py:163-174 — each initial row sorted by (score, draw position).
 // One warp per row, K <= 64 (two keys per lane above 32).
 template <int KPL>
-__global__ void sort_rows_kernel(const double *__restrict__ pts, const double *__restrict__ log64,
-                                 const double *__restrict__ xlogx, int d, int K, int64_t lo, int64_t hi,
-                                 const int32_t *__restrict__ draws, int32_t *__restrict__ out_ids,
+__global__ void sort_rows_kernel(const double *__restrict__ pts, int pstride, const double *__restrict__ log64,
+                                 int d64, const double *__restrict__ xlogx, int d, int metric, int K, int64_t lo,
+                                 int64_t hi, const int32_t *__restrict__ draws, int32_t *__restrict__ out_ids,
                                  double *__restrict__ out_kl) {
   extern __shared__ double sx[];  // per warp: d doubles
   const int lane = threadIdx.x & 31;
@@ -60,7 +98,7 @@ __global__ void sort_rows_kernel(const double *__restrict__ pts, const double *_
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t x = lo + (int64_t)blockIdx.x * (blockDim.x >> 5) + w; x < hi; x += warps) {
     const int64_t xr = x - lo;
-    for (int j = lane; j < d; j += 32) x64[j] = pts[x * d + j];
+    for (int j = lane; j < d; j += 32) x64[j] = pts[x * pstride + j];
     __syncwarp();
     const double xl = xlogx[x];
     KeyD key[KPL];
@@ -73,7 +111,7 @@ __global__ void sort_rows_kernel(const double *__restrict__ pts, const double *_
       if (pos < K) {
         int y = draws[xr * K + pos];
         idv[q] = y;
-        key[q] = {exact_score(x64, log64 + (int64_t)y * d, d, xl), pos};
+        key[q] = {exact_score_m(x64, log64 + (int64_t)y * d64, d, xl, metric), pos};
       }
     }
     // sort keys; the tie field is the draw position (stable argsort)
@@ -146,29 +184,55 @@ int knnd_kl_prepare(const double *points, int64_t n, int32_t d, int32_t ld32, fl
   return KNND_OK;
 }
 
-int knnd_batch_scores(const double *points, const double *log64, const double *xlogx, int64_t n,
-                      int32_t d, int64_t x, const int32_t *ids, int64_t m, double *out, void *stream) {
-  KNND_CHECK_ARG(points && log64 && xlogx && out, "knnd_batch_scores: null pointer");
-  KNND_CHECK_ARG(x >= 0 && x < n, "knnd_batch_scores: anchor %lld out of range", (long long)x);
-  KNND_CHECK_ARG(m >= 0, "knnd_batch_scores: m < 0");
-  if (m == 0) return KNND_OK;
-  KNND_CHECK_ARG(ids != nullptr, "knnd_batch_scores: null ids");
-  const int threads = 256;
-  int64_t blocks = (m + threads - 1) / threads;
-  if (blocks > (int64_t)num_sms() * 8) blocks = (int64_t)num_sms() * 8;
-  batch_scores_kernel<<<(unsigned)blocks, threads, d * sizeof(double), as_stream(stream)>>>(
-      points, log64, xlogx, d, x, ids, m, out);
+int knnd_l2_prepare(const double *vectors, const double *sq64, int64_t n, int32_t d, int32_t ld32,
+                    const double *center, float *cand32, float *anchor32, double *rows64, void *stream) {
+  KNND_CHECK_ARG(vectors && sq64 && center && cand32 && anchor32 && rows64, "knnd_l2_prepare: null pointer");
+  KNND_CHECK_ARG(n >= 1 && d >= 1, "knnd_l2_prepare: bad shape n=%lld d=%d", (long long)n, d);
+  KNND_CHECK_ARG(ld32 >= d + 1 && ld32 % 4 == 0, "knnd_l2_prepare: ld32=%d must be >= d+1 and a multiple of 4",
+                 ld32);
+  int64_t blocks = (n + 7) / 8;
+  if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+  l2_prepare_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(vectors, sq64, n, d, ld32, center, cand32,
+                                                                      anchor32, rows64);
   KNND_LAUNCHED(1);
   return KNND_OK;
 }
 
-int knnd_sort_rows(const double *points, const double *log64, const double *xlogx, int64_t n,
-                   int32_t d, int32_t k, int64_t row_lo, int64_t row_hi, const int32_t *draws,
-                   int32_t *out_ids, double *out_kl, void *stream) {
-  KNND_CHECK_ARG(points && log64 && xlogx && draws && out_ids, "knnd_sort_rows: null pointer");
-  KNND_CHECK_ARG(0 <= row_lo && row_lo <= row_hi && row_hi <= n, "knnd_sort_rows: bad row range");
+static int batch_scores_impl(const char *who, const double *pts, int pstride, const double *log64, int d64,
+                             const double *xlogx, int64_t n, int32_t d, int metric, int64_t x, const int32_t *ids,
+                             int64_t m, double *out, void *stream) {
+  KNND_CHECK_ARG(pts && log64 && xlogx && out, "%s: null pointer", who);
+  KNND_CHECK_ARG(x >= 0 && x < n, "%s: anchor %lld out of range", who, (long long)x);
+  KNND_CHECK_ARG(m >= 0, "%s: m < 0", who);
+  if (m == 0) return KNND_OK;
+  KNND_CHECK_ARG(ids != nullptr, "%s: null ids", who);
+  const int threads = 256;
+  int64_t blocks = (m + threads - 1) / threads;
+  if (blocks > (int64_t)num_sms() * 8) blocks = (int64_t)num_sms() * 8;
+  batch_scores_kernel<<<(unsigned)blocks, threads, d * sizeof(double), as_stream(stream)>>>(
+      pts, pstride, log64, d64, xlogx, d, metric, x, ids, m, out);
+  KNND_LAUNCHED(1);
+  return KNND_OK;
+}
+
+int knnd_batch_scores(const double *points, const double *log64, const double *xlogx, int64_t n,
+                      int32_t d, int64_t x, const int32_t *ids, int64_t m, double *out, void *stream) {
+  return batch_scores_impl("knnd_batch_scores", points, d, log64, d, xlogx, n, d, METRIC_KL, x, ids, m, out, stream);
+}
+
+int knnd_l2_batch_scores(const double *rows64, const double *sq64, int64_t n, int32_t d, int64_t x,
+                         const int32_t *ids, int64_t m, double *out, void *stream) {
+  return batch_scores_impl("knnd_l2_batch_scores", rows64, d + 1, rows64, d + 1, sq64, n, d, METRIC_L2, x, ids, m,
+                           out, stream);
+}
+
+static int sort_rows_impl(const char *who, const double *pts, int pstride, const double *log64, int d64,
+                          const double *xlogx, int64_t n, int32_t d, int metric, int32_t k, int64_t row_lo,
+                          int64_t row_hi, const int32_t *draws, int32_t *out_ids, double *out_kl, void *stream) {
+  KNND_CHECK_ARG(pts && log64 && xlogx && draws && out_ids, "%s: null pointer", who);
+  KNND_CHECK_ARG(0 <= row_lo && row_lo <= row_hi && row_hi <= n, "%s: bad row range", who);
   if (k < 1 || k > 64) {
-    set_error("knnd_sort_rows: K=%d unsupported (1..64)", k);
+    set_error("%s: K=%d unsupported (1..64)", who, k);
     return KNND_EUNSUPPORTED;
   }
   if (row_hi == row_lo) return KNND_OK;
@@ -179,12 +243,25 @@ int knnd_sort_rows(const double *points, const double *log64, const double *xlog
   size_t smem = (size_t)wpb * d * sizeof(double);
   if (k <= 32)
     sort_rows_kernel<1><<<(unsigned)blocks, threads, smem, as_stream(stream)>>>(
-        points, log64, xlogx, d, k, row_lo, row_hi, draws, out_ids, out_kl);
+        pts, pstride, log64, d64, xlogx, d, metric, k, row_lo, row_hi, draws, out_ids, out_kl);
   else
     sort_rows_kernel<2><<<(unsigned)blocks, threads, smem, as_stream(stream)>>>(
-        points, log64, xlogx, d, k, row_lo, row_hi, draws, out_ids, out_kl);
+        pts, pstride, log64, d64, xlogx, d, metric, k, row_lo, row_hi, draws, out_ids, out_kl);
   KNND_LAUNCHED(1);
   return KNND_OK;
+}
+
+int knnd_sort_rows(const double *points, const double *log64, const double *xlogx, int64_t n,
+                   int32_t d, int32_t k, int64_t row_lo, int64_t row_hi, const int32_t *draws,
+                   int32_t *out_ids, double *out_kl, void *stream) {
+  return sort_rows_impl("knnd_sort_rows", points, d, log64, d, xlogx, n, d, METRIC_KL, k, row_lo, row_hi, draws,
+                        out_ids, out_kl, stream);
+}
+
+int knnd_l2_sort_rows(const double *rows64, const double *sq64, int64_t n, int32_t d, int32_t k, int64_t row_lo,
+                      int64_t row_hi, const int32_t *draws, int32_t *out_ids, double *out_d2, void *stream) {
+  return sort_rows_impl("knnd_l2_sort_rows", rows64, d + 1, rows64, d + 1, sq64, n, d, METRIC_L2, k, row_lo,
+                        row_hi, draws, out_ids, out_d2, stream);
 }
 
 int knnd_fcc(const int32_t *friends, int64_t n, int32_t k, const int32_t *xs, const int32_t *is,

@@ -89,17 +89,12 @@ class CudaOps:
              tally: torch.Tensor, out_kl: torch.Tensor | None = None, out_ucount: torch.Tensor | None = None,
              flags: int | None = None, bound_in: torch.Tensor | None = None,
              bound_out: torch.Tensor | None = None) -> None:
+        """knnd_local_join (KL) / knnd_l2_local_join (Euclidean), by the tables' metric."""
         if flags is None:
-            flags = _lib.JOIN_NONPOS_LOG if tabs.max_coord <= 1.0 else 0
-        nbytes = _lib.load().knnd_local_join_workspace_bytes(n, tabs.d, k, csr.lo, csr.hi, max_indeg)
+            flags = tabs.join_flags()
+        nbytes = _lib.load().knnd_local_join_workspace_bytes(n, tabs.dplan, k, csr.lo, csr.hi, max_indeg)
         ws = self._workspace("join", nbytes)
-        _lib.call("knnd_local_join", tabs.points.data_ptr(), tabs.log32.data_ptr(), tabs.log64.data_ptr(),
-                  tabs.xlogx.data_ptr(), n, tabs.d, tabs.ld, table.data_ptr(), k, csr.indptr.data_ptr(),
-                  csr.indices.data_ptr(), csr.lo, csr.hi, max_indeg, out_rows.data_ptr(),
-                  out_kl.data_ptr() if out_kl is not None else None,
-                  out_ucount.data_ptr() if out_ucount is not None else None, tally.data_ptr(),
-                  bound_in.data_ptr() if bound_in is not None else None,
-                  bound_out.data_ptr() if bound_out is not None else None, ws.data_ptr(), ws.numel(), flags,
+        tabs.join(table, k, csr, max_indeg, out_rows, tally, out_kl, out_ucount, bound_in, bound_out, ws, flags,
                   self._stream())
 
     def random_kout(self, state: tuple, n: int, k: int, table: torch.Tensor, out_meta: torch.Tensor,
@@ -121,9 +116,7 @@ class CudaOps:
 
     def sort_rows(self, tabs, rows: torch.Tensor, k: int, lo: int, hi: int, out_kl: torch.Tensor | None = None):
         # in place: each warp reads its row before writing it back
-        _lib.call("knnd_sort_rows", tabs.points.data_ptr(), tabs.log64.data_ptr(), tabs.xlogx.data_ptr(), tabs.n,
-                  tabs.d, k, lo, hi, rows.data_ptr(), rows.data_ptr(),
-                  out_kl.data_ptr() if out_kl is not None else None, self._stream())
+        tabs.sort_rows(rows, k, lo, hi, out_kl, self._stream())
 
 
 @dataclass

@@ -6,7 +6,7 @@ the reference's names, arguments and results: row x of the exact graph is the
 K smallest (fp64 score, id) over every other point (evaluation.py:83-90, the
 ``_smallest_k`` order of evaluation.py:53-71).  ``exact_rows`` is the same
 computation for a subset of anchors — what a sampled recall at n = 1M needs.
-Only the KL ranking system is accelerated (no CPU fallback); the
+The KL and Euclidean ranking systems are accelerated (no CPU fallback); the
 metrizability checker (evaluation.py:140-) is out of scope.
 """
 
@@ -49,12 +49,7 @@ def _exact_call(tabs, q: torch.Tensor, k: int, cap: int, ids: torch.Tensor, scor
                 count: torch.Tensor) -> None:
     nbytes = _lib.load().knnd_exact_knn_workspace_bytes(q.numel(), cap)
     ws = torch.empty(nbytes, dtype=torch.uint8, device=tabs.device)
-    flags = _lib.JOIN_NONPOS_LOG if tabs.max_coord <= 1.0 else 0
-    stream = torch.cuda.current_stream(tabs.device).cuda_stream
-    _lib.call("knnd_exact_knn", tabs.points.data_ptr(), tabs.log32.data_ptr(), tabs.log64.data_ptr(),
-              tabs.xlogx.data_ptr(), tabs.n, tabs.d, tabs.ld, q.data_ptr(), q.numel(), k, cap, ids.data_ptr(),
-              scores.data_ptr() if scores is not None else None, count.data_ptr(), ws.data_ptr(), ws.numel(),
-              flags, stream)
+    tabs.exact(q, k, cap, ids, scores, count, ws, torch.cuda.current_stream(tabs.device).cuda_stream)
 
 
 def exact_rows_device(rs, queries, k: int, device=None, with_scores: bool = False):
