@@ -45,7 +45,7 @@ struct ExactParams {
   int d64;         // fp64 row length (d, or d+1 for L2)
   int pstride;     // row stride of `points`
   const float *aside32;  // L2: anchor-side fp32 rows (null for KL)
-  double gamma, maxnorm;  // L2: absolute error scale of the fp64 values (join.cu exact_slack)
+  float slack;            // L2: absolute error bound of the fp64 values (join.cu JoinParams::slack)
 };
 
 template <int NV4, int Q, bool ABS>
@@ -228,12 +228,7 @@ __global__ void __launch_bounds__(XWARPS * 32) exact_screen_kernel(ExactParams p
           float a = am[qq];
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) a = fmaxf(a, __shfl_xor_sync(FULL, a, o));
-          float slack = 0.f;
-          if (p.metric == METRIC_L2 && qid[qq] >= 0) {
-            const double r = sqrt(fmax(p.xlogx[qid[qq]], 0.0)) + p.maxnorm;
-            slack = (float)(p.gamma * r * r);
-          }
-          th = T + 2.f * (p.band * a + slack) + fabsf(T) * 1e-6f;
+          th = T + 2.f * (p.band * a + p.slack) + fabsf(T) * 1e-6f;
         }
         theta[qq] = qid[qq] >= 0 ? th : -__int_as_float(0x7f800000);  // padding queries take nothing
       }
@@ -416,8 +411,7 @@ int knnd_l2_exact_knn(const float *anchor32, const float *cand32, const double *
   p.d64 = d + 1;
   p.pstride = d + 1;
   p.aside32 = anchor32;
-  p.gamma = (d + 4) * 0x1p-53;
-  p.maxnorm = maxnorm;
+  p.slack = (float)((d + 4) * 0x1p-53 * 4.0 * maxnorm * maxnorm);
   return exact_run("knnd_l2_exact_knn", p, d + 1, k, ws, ws_bytes, stream);
 }
 

@@ -64,17 +64,11 @@ struct JoinParams {
   int d64;                               // fp64 row length of log64 (d; d+1 for L2: the vector, then |v|^2)
   int pstride;                           // row stride of `points` (the anchor's fp64 coordinates)
   const float *__restrict__ aside32;     // L2: anchor-side fp32 rows (2(x-mu), -1); KL: null (from points)
-  double gamma;                          // L2: |our fp64 d2 - true d2| <= gamma (|x| + maxnorm)^2
-  double maxnorm;
+  // absolute error bound of the exact fp64 values (0 for KL, whose error is
+  // relative and inside `band`; L2: (d+4) 2^-53 (2 maxnorm)^2 >= |fl(d2) - d2|);
+  // the screen band of an anchor is 2 (band * am + slack)
+  float slack;
 };
-
-// absolute slack of the exact fp64 values (0 for KL, whose error is relative
-// and inside p.band); the screen band of an anchor is 2 (band*am + slack)
-__device__ __forceinline__ float exact_slack(const JoinParams &p, double xl) {
-  if (p.metric != METRIC_L2) return 0.f;
-  const double r = sqrt(fmax(xl, 0.0)) + p.maxnorm;
-  return (float)(p.gamma * r * r);
-}
 
 __host__ __device__ inline size_t al16(size_t v) { return (v + 15) & ~(size_t)15; }
 
@@ -518,9 +512,11 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     }
     for (int i = tid; i < 2 * NBIN; i += G) hist[i] = 0;
     for (int i = tid; i < nS; i += G) S[i] = i < K ? __ldg(p.F + (int64_t)x * K + i) : __ldg(p.indices + c0 + (i - K));
-    for (int i = tid; i < ld; i += G)
-      x32[i] = p.aside32 ? __ldg(p.aside32 + (int64_t)x * ld + i)
-                         : (i < d ? (float)__ldg(p.points + (int64_t)x * p.pstride + i) : 0.f);
+    if (p.aside32) {
+      for (int i = tid; i < ld; i += G) x32[i] = __ldg(p.aside32 + (int64_t)x * ld + i);
+    } else {
+      for (int i = tid; i < ld; i += G) x32[i] = i < d ? (float)__ldg(p.points + (int64_t)x * p.pstride + i) : 0.f;
+    }
     for (int i = tid; i < d; i += G) x64[i] = __ldg(p.points + (int64_t)x * p.pstride + i);
     if (tid == 0) {
       hdr[0] = 0;
@@ -572,7 +568,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
       wstage = reinterpret_cast<float *>(table + u4) + (size_t)warp * per_warp_floats;
     }
     float mn = __int_as_float(0x7f800000), mx = -mn, am = 0.f;
-    const float slack = exact_slack(p, __ldg(p.xlogx + x));
+    const float slack = p.slack;
     float best0 = mn, best1 = mn;  // this lane's two smallest screened values
     float4 xreg[NV4 > 0 ? NV4 : 1];  // the anchor's fp32 row in registers
     if constexpr (NV4 > 0) {
@@ -849,9 +845,11 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
       for (int i = lane; i < (H >> 2); i += 32) t4[i] = make_int4(EMPTY, EMPTY, EMPTY, EMPTY);
     }
     for (int i = lane; i < nS; i += 32) S[i] = i < K ? __ldg(p.F + (int64_t)x * K + i) : __ldg(p.indices + c0 + (i - K));
-    for (int i = lane; i < ld; i += 32)
-      x32[i] = p.aside32 ? __ldg(p.aside32 + (int64_t)x * ld + i)
-                         : (i < d ? (float)__ldg(p.points + (int64_t)x * p.pstride + i) : 0.f);
+    if (p.aside32) {
+      for (int i = lane; i < ld; i += 32) x32[i] = __ldg(p.aside32 + (int64_t)x * ld + i);
+    } else {
+      for (int i = lane; i < ld; i += 32) x32[i] = i < d ? (float)__ldg(p.points + (int64_t)x * p.pstride + i) : 0.f;
+    }
     for (int i = lane; i < d; i += 32) x64[i] = __ldg(p.points + (int64_t)x * p.pstride + i);
     __syncwarp();
     float4 xreg[NV4 > 0 ? NV4 : 1];  // the anchor's fp32 row in registers
@@ -916,7 +914,7 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
 #pragma unroll
     for (int q = 0; q < Q; ++q) best[q] = __int_as_float(0x7f800000);
     float am = 0.f;
-    const float slack = exact_slack(p, __ldg(p.xlogx + x));
+    const float slack = p.slack;
     // ids of batch b+1 are in a register while batch b computes; batch b+2's are being loaded
     // two staging buffers in the table past the scores ([0, U), U <= H/2)
     const int u4 = (U + 3) & ~3;
@@ -1482,8 +1480,7 @@ int knnd_l2_local_join(const float *anchor32, const float *cand32, const double 
   p.d64 = d + 1;
   p.pstride = d + 1;
   p.aside32 = anchor32;
-  p.gamma = (d + 4) * 0x1p-53;
-  p.maxnorm = maxnorm;
+  p.slack = (float)((d + 4) * 0x1p-53 * 4.0 * maxnorm * maxnorm);
   return join_run("knnd_l2_local_join", p, n, d + 1, k, row_lo, row_hi, max_indeg, ws, ws_bytes, stream);
 }
 
