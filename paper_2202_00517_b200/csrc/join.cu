@@ -773,7 +773,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
 //     a valid T (tight unless one lane holds > 2*KPL of the best K)
 
 struct WarpSlab {
-  size_t x32, x64, S, table, list, total;
+  size_t x32, x64, S, pre, table, list, total;  // (x32, x64, S) twice, `pre` bytes apart
 };
 
 __host__ __device__ inline WarpSlab warp_slab(int d, int ld, int H, int SW) {
@@ -785,12 +785,27 @@ __host__ __device__ inline WarpSlab warp_slab(int d, int ld, int H, int SW) {
   o = al16(o + (size_t)d * 8);
   L.S = o;
   o = al16(o + (size_t)SW * 4);
+  L.pre = o;  // one anchor's inputs; the next anchor's are prefetched into the second copy
+  o *= 2;
   L.table = o;
   o = al16(o + (size_t)H * 4);
   L.list = o;
   o = al16(o + (size_t)(H / 2) * 4);
   L.total = o;
   return L;
+}
+
+// cp.async the inputs of anchor x (S = F(x) then C(x); its fp64 row; for L2 its
+// fp32 anchor-side row) into one input buffer of a warp slab
+__device__ __forceinline__ void prefetch_anchor(const JoinParams &p, int x, int64_t c0, int c, int32_t *S,
+                                                float *x32, double *x64, int lane) {
+  const int K = p.K;
+  for (int i = lane; i < K + c; i += 32)
+    cp_async4(S + i, i < K ? p.F + (int64_t)x * K + i : p.indices + c0 + (i - K));
+  for (int i = lane; i < p.d; i += 32) cp_async8(x64 + i, p.points + (int64_t)x * p.pstride + i);
+  if (p.aside32)
+    for (int i = lane; i < p.ld / 4; i += 32) cp_async16(x32 + 4 * i, p.aside32 + (int64_t)x * p.ld + 4 * i);
+  cp_async_commit();
 }
 
 template <int NV4, int KPL, bool GLIST>
@@ -804,9 +819,6 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
   const unsigned shift = 32u - (unsigned)logH;
   const WarpSlab L = warp_slab(p.d, p.ld, H, SW);
   unsigned char *base = sm + (size_t)warp * (GLIST ? L.list : L.total);  // GLIST: no list in smem
-  float *x32 = reinterpret_cast<float *>(base + L.x32);
-  double *x64 = reinterpret_cast<double *>(base + L.x64);
-  int32_t *S = reinterpret_cast<int32_t *>(base + L.S);
   int32_t *table = reinterpret_cast<int32_t *>(base + L.table);
   int32_t *list = GLIST ? glists + (size_t)(blockIdx.x * (blockDim.x >> 5) + warp) * (H >> 1)
                         : reinterpret_cast<int32_t *>(base + L.list);
@@ -820,22 +832,42 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
   unsigned long long acc_comp = 0, acc_changed = 0, acc_bad = 0;
   const int count = *acount;
   int *cursor = const_cast<int *>(acount) + 8;  // dynamic anchor fetch, 4 anchors per atomic
-  int a_base = 0, a_left = 0;
+  // The next anchor is known one anchor ahead: its id is loaded when the
+  // current one starts, its CSR range after the dedup, and its inputs (S and
+  // rows) are cp.async'd into the other input buffer after the screen, so the
+  // load chain alist -> indptr -> S -> F(S) is off the critical path.
+  auto fetch4 = [&]() {
+    int got = 0;
+    if (lane == 0) got = atomicAdd(cursor, 4);
+    return __shfl_sync(FULL, got, 0);
+  };
+  int a = fetch4(), a_rem = 3;
+  int x = -1, c = 0;
+  int64_t c0 = 0;
+  int pb = 0;
+  if (a < count) {
+    x = alist[a];
+    c0 = p.indptr[(int64_t)x - p.lo];
+    c = (int)(p.indptr[(int64_t)x - p.lo + 1] - c0);
+    prefetch_anchor(p, x, c0, c, reinterpret_cast<int32_t *>(base + L.S), reinterpret_cast<float *>(base + L.x32),
+                    reinterpret_cast<double *>(base + L.x64), lane);
+  }
 
-  for (;;) {
-    if (a_left == 0) {
-      int got = 0;
-      if (lane == 0) got = atomicAdd(cursor, 4);
-      a_base = __shfl_sync(FULL, got, 0);
-      a_left = 4;
+  while (a < count) {
+    int a_nxt;
+    if (a_rem > 0) {
+      a_nxt = a + 1;
+      --a_rem;
+    } else {
+      a_nxt = fetch4();
+      a_rem = 3;
     }
-    const int a = a_base++;
-    --a_left;
-    if (a >= count) break;
-    const int x = alist[a];
+    const int xn = a_nxt < count ? __ldg(alist + a_nxt) : -1;  // consumed after the dedup
+    unsigned char *inb = base + (size_t)pb * L.pre;
+    float *x32 = reinterpret_cast<float *>(inb + L.x32);
+    double *x64 = reinterpret_cast<double *>(inb + L.x64);
+    int32_t *S = reinterpret_cast<int32_t *>(inb + L.S);
     const int64_t xr = (int64_t)x - p.lo;
-    const int64_t c0 = p.indptr[xr];
-    const int c = (int)(p.indptr[xr + 1] - c0);
     const int nS = K + c;
     const int total = nS * K1;
 
@@ -844,13 +876,10 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
       int4 *t4 = reinterpret_cast<int4 *>(table);
       for (int i = lane; i < (H >> 2); i += 32) t4[i] = make_int4(EMPTY, EMPTY, EMPTY, EMPTY);
     }
-    for (int i = lane; i < nS; i += 32) S[i] = i < K ? __ldg(p.F + (int64_t)x * K + i) : __ldg(p.indices + c0 + (i - K));
-    if (p.aside32) {
-      for (int i = lane; i < ld; i += 32) x32[i] = __ldg(p.aside32 + (int64_t)x * ld + i);
-    } else {
-      for (int i = lane; i < ld; i += 32) x32[i] = i < d ? (float)__ldg(p.points + (int64_t)x * p.pstride + i) : 0.f;
-    }
-    for (int i = lane; i < d; i += 32) x64[i] = __ldg(p.points + (int64_t)x * p.pstride + i);
+    cp_async_wait_all();  // this anchor's prefetched inputs
+    __syncwarp();
+    if (!p.aside32)
+      for (int i = lane; i < ld; i += 32) x32[i] = i < d ? (float)x64[i] : 0.f;
     __syncwarp();
     float4 xreg[NV4 > 0 ? NV4 : 1];  // the anchor's fp32 row in registers
     if constexpr (NV4 > 0) {
@@ -908,6 +937,12 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
       }
     }
     __syncwarp();
+
+    int64_t nc0 = 0, nc1 = 0;
+    if (xn >= 0) {
+      nc0 = __ldg(p.indptr + ((int64_t)xn - p.lo));
+      nc1 = __ldg(p.indptr + ((int64_t)xn - p.lo + 1));
+    }
 
     // ---- phase 2: screen; per-lane Q smallest, max |x log y| sum
     float best[Q];
@@ -968,6 +1003,11 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
         }
       }
       __syncwarp();
+    }
+    if (xn >= 0) {  // the staging groups are complete: start the next anchor's inputs
+      unsigned char *nb = base + (size_t)(pb ^ 1) * L.pre;
+      prefetch_anchor(p, xn, nc0, (int)(nc1 - nc0), reinterpret_cast<int32_t *>(nb + L.S),
+                      reinterpret_cast<float *>(nb + L.x32), reinterpret_cast<double *>(nb + L.x64), lane);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) am = fmaxf(am, __shfl_xor_sync(FULL, am, o));
@@ -1045,7 +1085,13 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
       if (p.out_ucount) p.out_ucount[xr] = U;
     }
     __syncwarp();
+    a = a_nxt;
+    x = xn;
+    c0 = nc0;
+    c = (int)(nc1 - nc0);
+    pb ^= 1;
   }
+  cp_async_wait_all();
   if (lane == 0) {
     if (acc_comp) atomicAdd(&p.tally[0], acc_comp);
     if (acc_changed) atomicAdd(&p.tally[1], acc_changed);
