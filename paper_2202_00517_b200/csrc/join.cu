@@ -319,6 +319,17 @@ __device__ __forceinline__ void exact_rank(const JoinParams &p, WarpTopK<KeyD, K
   }
 }
 
+// The fp64 fallback of phase 4: rescore R, write the row, return the change
+// flag.  (Kept inline: an out-of-line call measured slower — the call saves
+// and restores the live registers.)
+template <int KPL>
+__device__ __forceinline__ bool exact_row(const JoinParams &p, const int32_t *ids, int nR, double *stage64, int rcap,
+                                       const double *x64, int x, int64_t xr, int lane) {
+  WarpTopK<KeyD, KPL> ex;
+  exact_rank<KPL>(p, ex, ids, nR, stage64, rcap, x64, __ldg(p.xlogx + x), lane);
+  return emit_row<KPL>(p, ex, x, xr, lane);
+}
+
 // Phase 4 without fp64 when the screen already decides the row: sort R (<= 32)
 // by (screened value, id); if each of the first K screened values is below the
 // next one by more than the error band 2c*am (+ margin), the exact order of the
@@ -740,9 +751,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
       float kth = theta;  // every member of the new row has a screened value <= theta
       if (!(KPL == 1 && p.out_kl == nullptr && nR <= 32 &&
             certify_row(p, R, rval, nR, 2.f * (p.band * am + slack), x, xr, lane, diff, kth))) {
-        WarpTopK<KeyD, KPL> ex;
-        exact_rank<KPL>(p, ex, R, nR, stage64, rcap64, x64, __ldg(p.xlogx + x), lane);
-        diff = emit_row<KPL>(p, ex, x, xr, lane);
+        diff = exact_row<KPL>(p, R, nR, stage64, rcap64, x64, x, xr, lane);
       }
       if (p.bound_out && lane == 0) p.bound_out[xr] = kth;
       if (lane == 0) {
@@ -800,10 +809,13 @@ __host__ __device__ inline WarpSlab warp_slab(int d, int ld, int H, int SW) {
 __device__ __forceinline__ void prefetch_anchor(const JoinParams &p, int x, int64_t c0, int c, int32_t *S,
                                                 float *x32, double *x64, int lane) {
   const int K = p.K;
+#pragma unroll 1
   for (int i = lane; i < K + c; i += 32)
     cp_async4(S + i, i < K ? p.F + (int64_t)x * K + i : p.indices + c0 + (i - K));
+#pragma unroll 1
   for (int i = lane; i < p.d; i += 32) cp_async8(x64 + i, p.points + (int64_t)x * p.pstride + i);
   if (p.aside32)
+#pragma unroll 1
     for (int i = lane; i < p.ld / 4; i += 32) cp_async16(x32 + 4 * i, p.aside32 + (int64_t)x * p.ld + 4 * i);
   cp_async_commit();
 }
@@ -891,18 +903,19 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
     int U = 0;
     {
       int s = s_init, j = j_init;
-      // pre-dedup ids two groups ahead; the friend-row loads stay in flight until
-      // their group is consumed (the select below is deferred to that point)
-      int gf[2][UNR1], gv[2][UNR1], gm[2][UNR1];  // loaded friend id, S value, mode (0 out, 1 self, 2 friend)
-      auto load_group = [&](int slot, int e0) {
+      // Pre-dedup ids two groups ahead: the friend-row loads stay in flight until
+      // their group is consumed (the select is deferred to that point).  Slot A
+      // is consumed, slot B rotates into A, the group two ahead loads into B —
+      // one copy of the loop body (the kernel is instruction-fetch sensitive).
+      int fA[UNR1], vA[UNR1], fB[UNR1], vB[UNR1];  // friend id loaded; S value, or -1 (out) / -2 (use friend)
+      auto load_group = [&](int (&f)[UNR1], int (&v)[UNR1], int e0) {
 #pragma unroll
         for (int u = 0; u < UNR1; ++u) {
           const int e = e0 + u * 32 + lane;
           const bool in = e < total;
-          const int v = S[in ? s : 0];
-          gf[slot][u] = __ldg(p.F + (int64_t)v * K + (j > 0 ? j - 1 : 0));
-          gv[slot][u] = v;
-          gm[slot][u] = in ? (j == 0 ? 1 : 2) : 0;
+          const int sv = S[in ? s : 0];
+          f[u] = __ldg(p.F + (int64_t)sv * K + (j > 0 ? j - 1 : 0));
+          v[u] = in ? (j == 0 ? sv : -2) : -1;
           s += Gq;
           j += Gr;
           const bool wrap = j >= K1;
@@ -910,12 +923,23 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
           s += wrap ? 1 : 0;
         }
       };
-      // one group: ids from slot `g` (a compile-time constant after inlining)
-      auto process = [&](const int g, const int e0) {
+      load_group(fA, vA, 0);
+      load_group(fB, vB, 32 * UNR1);
+#pragma unroll 1
+      for (int e0 = 0; e0 < total; e0 += 32 * UNR1) {
         int id[UNR1];
 #pragma unroll
-        for (int u = 0; u < UNR1; ++u) id[u] = gm[g][u] == 0 ? -1 : (gm[g][u] == 1 ? gv[g][u] : gf[g][u]);
-        if (e0 + 64 * UNR1 < total) load_group(g, e0 + 64 * UNR1);  // two groups ahead
+        for (int u = 0; u < UNR1; ++u) {
+          id[u] = vA[u] == -2 ? fA[u] : vA[u];
+          fA[u] = fB[u];
+          vA[u] = vB[u];
+        }
+        if (e0 + 64 * UNR1 < total) {
+          load_group(fB, vB, e0 + 64 * UNR1);
+        } else {
+#pragma unroll
+          for (int u = 0; u < UNR1; ++u) vB[u] = -1;
+        }
         // shared-memory CAS insert (hash_insert_cas): in-warp duplicates resolve in
         // the CAS itself; the ballots append the winners in lane order
         bool nw[UNR1];
@@ -928,12 +952,6 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
           if (nw[u]) list[U + __popc(m & lanemask_lt())] = id[u];
           U += __popc(m);
         }
-      };
-      load_group(0, 0);
-      if (32 * UNR1 < total) load_group(1, 32 * UNR1);
-      for (int e0 = 0; e0 < total; e0 += 64 * UNR1) {
-        process(0, e0);
-        if (e0 + 32 * UNR1 < total) process(1, e0 + 32 * UNR1);
       }
     }
     __syncwarp();
@@ -1073,9 +1091,7 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
     float kth = theta;  // every member of the new row has a screened value <= theta
     if (!(KPL == 1 && p.out_kl == nullptr && nR <= 32 &&
           certify_row(p, list, scores, nR, 2.f * (p.band * am + slack), x, xr, lane, diff, kth))) {
-      WarpTopK<KeyD, KPL> ex;
-      exact_rank<KPL>(p, ex, list, nR, stage64, rcap64, x64, __ldg(p.xlogx + x), lane);
-      diff = emit_row<KPL>(p, ex, x, xr, lane);
+      diff = exact_row<KPL>(p, list, nR, stage64, rcap64, x64, x, xr, lane);
     }
     if (p.bound_out && lane == 0) p.bound_out[xr] = kth;
     if (lane == 0) {
