@@ -385,7 +385,7 @@ __device__ __forceinline__ void collect_r(const float *scores, const int32_t *li
 }
 
 struct SmemLayout {
-  size_t x32, x64, red, hist, rval, stage, S, table, list, total;
+  size_t x32, x64, S, pre, red, hist, rval, stage, table, list, total;  // (x32, x64[, S]) twice, `pre` apart
 };
 
 constexpr int NBIN = 256;        // histogram-select buckets per pass
@@ -393,11 +393,18 @@ constexpr int LSTAGE_ROWS = 16;  // per-warp staged rows in the global-table cla
 
 __host__ __device__ inline SmemLayout smem_layout(int G, bool gtab, int d, int ld, int H, int SW) {
   SmemLayout L;
-  size_t o = 64;  // header ints: [0] |U| [1] |R| [2] b1 [3] before1 [4] b2
+  size_t o = 64;  // header ints: [0] |U| [1] |R| [2] b1 [3] before1 [4] b2, [8..12] next anchor
   L.x32 = o;
   o = al16(o + (size_t)ld * 4);
   L.x64 = o;
   o = al16(o + (size_t)d * 8);
+  L.S = 0;
+  if (!gtab) {
+    L.S = o;
+    o = al16(o + (size_t)SW * 4);
+  }
+  L.pre = o - L.x32;  // one anchor's inputs; the next anchor's are prefetched into the second copy
+  o += L.pre;
   L.red = o;
   o = al16(o + (size_t)(G / 32) * 4 * 4);
   L.hist = o;
@@ -406,19 +413,17 @@ __host__ __device__ inline SmemLayout smem_layout(int G, bool gtab, int d, int l
   o = al16(o + 32 * 4);
   if (!gtab) {
     L.stage = 0;  // staging uses the (dead) table
-    L.S = o;
-    o = al16(o + (size_t)SW * 4);
     L.table = o;
     o = al16(o + (size_t)H * 4);
     L.list = o;
     o = al16(o + (size_t)(H / 2) * 4);
   } else {
     size_t st = (size_t)(G / 32) * LSTAGE_ROWS * ld * 4;
-    const size_t st64 = (size_t)32 * (d | 1) * 8;
+    const size_t st64 = (size_t)32 * ((d + 1) | 1) * 8;  // fp64 rows of d (KL) or d+1 (L2) doubles
     if (st < st64) st = st64;
     L.stage = o;
     o = al16(o + st);
-    L.S = L.table = L.list = 0;
+    L.table = L.list = 0;
   }
   L.total = o;
   return L;
@@ -468,19 +473,17 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
   const unsigned shift = 32u - (unsigned)logH;
   const SmemLayout L = smem_layout(G, GTAB, p.d, p.ld, H, SW);
   int *hdr = reinterpret_cast<int *>(sm);
-  float *x32 = reinterpret_cast<float *>(sm + L.x32);
-  double *x64 = reinterpret_cast<double *>(sm + L.x64);
   float *red = reinterpret_cast<float *>(sm + L.red);
   int *hist = reinterpret_cast<int *>(sm + L.hist);
   int *hist2 = hist + NBIN;
   float *rval = reinterpret_cast<float *>(sm + L.rval);
-  int32_t *S, *table, *list;
+  int32_t *slabS = nullptr, *table, *list;
   float *wstage;  // this warp's fp32 staging rows
   double *stage64;
   int wrows, rcap64;
   if constexpr (GTAB) {
     int32_t *slab = gslab + (int64_t)blockIdx.x * slab_ints;
-    S = slab;
+    slabS = slab;
     table = slab + SW;
     list = table + H;
     wrows = LSTAGE_ROWS / 2;  // two buffers per warp
@@ -488,7 +491,6 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     stage64 = reinterpret_cast<double *>(sm + L.stage);
     rcap64 = 32;
   } else {
-    S = reinterpret_cast<int32_t *>(sm + L.S);
     table = reinterpret_cast<int32_t *>(sm + L.table);
     list = reinterpret_cast<int32_t *>(sm + L.list);
     wrows = 0;  // set per anchor (the staging area follows the scores)
@@ -503,35 +505,80 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
   unsigned long long acc_comp = 0, acc_changed = 0, acc_bad = 0;
   const int count = *acount;
   int *cursor = const_cast<int *>(acount) + 8;  // dynamic anchor fetch (zeroed with the counts)
-  if (tid == 0) hdr[8] = atomicAdd(cursor, 1);
+  // The next anchor is fetched one anchor ahead: thread 0 takes its index at the
+  // top, loads its id during phase 0 and its CSR range during the dedup, and
+  // publishes them in hdr[8..12] after the screen; every thread then cp.asyncs
+  // its inputs (S, rows) into the other input buffer while this anchor finishes.
+  int64_t *hdr64 = reinterpret_cast<int64_t *>(hdr + 10);
+  auto inputs = [&](int b, int32_t *&S, float *&x32, double *&x64) {
+    unsigned char *ib = sm + (size_t)b * L.pre;
+    x32 = reinterpret_cast<float *>(ib + L.x32);
+    x64 = reinterpret_cast<double *>(ib + L.x64);
+    S = GTAB ? slabS : reinterpret_cast<int32_t *>(ib + L.S);
+  };
+  auto prefetch = [&](int b, int xp, int64_t cp0, int cp) {
+    int32_t *S;
+    float *x32;
+    double *x64;
+    inputs(b, S, x32, x64);
+    if constexpr (!GTAB) {
+#pragma unroll 1
+      for (int i = tid; i < K + cp; i += G)
+        cp_async4(S + i, i < K ? p.F + (int64_t)xp * K + i : p.indices + cp0 + (i - K));
+    }
+#pragma unroll 1
+    for (int i = tid; i < d; i += G) cp_async8(x64 + i, p.points + (int64_t)xp * p.pstride + i);
+    if (p.aside32)
+#pragma unroll 1
+      for (int i = tid; i < ld / 4; i += G) cp_async16(x32 + 4 * i, p.aside32 + (int64_t)xp * ld + 4 * i);
+    cp_async_commit();
+  };
+  if (tid == 0) {
+    const int a0 = atomicAdd(cursor, 1);
+    hdr[8] = a0;
+    if (a0 < count) {
+      const int x0 = alist[a0];
+      hdr[9] = x0;
+      hdr64[0] = p.indptr[(int64_t)x0 - p.lo];
+      hdr[12] = (int)(p.indptr[(int64_t)x0 - p.lo + 1] - hdr64[0]);
+    }
+  }
   __syncthreads();
+  if (hdr[8] < count) prefetch(0, hdr[9], hdr64[0], hdr[12]);
+  int pb = 0;
 
   for (int a = hdr[8]; a < count; a = hdr[8]) {
-    const int x = alist[a];
+    const int x = hdr[9];
     const int64_t xr = (int64_t)x - p.lo;
-    const int64_t c0 = p.indptr[xr];
-    const int c = (int)(p.indptr[xr + 1] - c0);
+    const int64_t c0 = hdr64[0];
+    const int c = hdr[12];
     const int nS = K + c;
     const int total = nS * K1;
-    __syncthreads();  // everyone has read hdr[8]
-    if (tid == 0) hdr[8] = atomicAdd(cursor, 1);  // the next anchor, published by a later barrier
+    int32_t *S;
+    float *x32;
+    double *x64;
+    inputs(pb, S, x32, x64);
+    int an = 0, xn = -1;
+    int64_t nc0 = 0, nc1 = 0;
+    if (tid == 0) an = atomicAdd(cursor, 1);  // used after phase 0 (latency off the path)
+    cp_async_wait_all();
+    __syncthreads();  // this anchor's inputs are in buffer pb; everyone has read hdr[8..12]
 
-    // ---- phase 0: clear table + histograms, stage S and the anchor row
+    // ---- phase 0: clear table + histograms (S and the anchor rows were prefetched)
     {
       int4 *t4 = reinterpret_cast<int4 *>(table);
       for (int i = tid; i < (H >> 2); i += G) t4[i] = make_int4(EMPTY, EMPTY, EMPTY, EMPTY);
     }
     for (int i = tid; i < 2 * NBIN; i += G) hist[i] = 0;
-    for (int i = tid; i < nS; i += G) S[i] = i < K ? __ldg(p.F + (int64_t)x * K + i) : __ldg(p.indices + c0 + (i - K));
-    if (p.aside32) {
-      for (int i = tid; i < ld; i += G) x32[i] = __ldg(p.aside32 + (int64_t)x * ld + i);
-    } else {
-      for (int i = tid; i < ld; i += G) x32[i] = i < d ? (float)__ldg(p.points + (int64_t)x * p.pstride + i) : 0.f;
-    }
-    for (int i = tid; i < d; i += G) x64[i] = __ldg(p.points + (int64_t)x * p.pstride + i);
+    if constexpr (GTAB)
+      for (int i = tid; i < nS; i += G)
+        S[i] = i < K ? __ldg(p.F + (int64_t)x * K + i) : __ldg(p.indices + c0 + (i - K));
+    if (!p.aside32)
+      for (int i = tid; i < ld; i += G) x32[i] = i < d ? (float)x64[i] : 0.f;
     if (tid == 0) {
       hdr[0] = 0;
       hdr[1] = 0;
+      if (an < count) xn = __ldg(alist + an);
     }
     __syncthreads();
 
@@ -564,6 +611,10 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
           warp_append(isnew, y, &hdr[0], list, lane);
         }
       }
+    }
+    if (tid == 0 && xn >= 0) {
+      nc0 = __ldg(p.indptr + ((int64_t)xn - p.lo));
+      nc1 = __ldg(p.indptr + ((int64_t)xn - p.lo + 1));
     }
     __syncthreads();
     const int U = hdr[0];
@@ -635,6 +686,12 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
         }
         __syncwarp();
       }
+    }
+    if (tid == 0) {  // publish the next anchor (read after the threshold section's barrier)
+      hdr[8] = an;
+      hdr[9] = xn;
+      hdr64[0] = nc0;
+      hdr[12] = (int)(nc1 - nc0);
     }
     float T;
     int32_t *R = table + (H >> 1);
@@ -737,6 +794,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
       }
     }
     const float theta = T + 2.f * (p.band * am + slack) + fabsf(T) * 1e-6f;
+    if (hdr[8] < count) prefetch(pb ^ 1, hdr[9], hdr64[0], hdr[12]);
 
     // ---- phase 3: collect every candidate the screen cannot exclude
     if (!collected) {
@@ -762,7 +820,9 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
       }
     }
     __syncthreads();
+    pb ^= 1;
   }
+  cp_async_wait_all();
   if (tid == 0) {
     if (acc_comp) atomicAdd(&p.tally[0], acc_comp);
     if (acc_changed) atomicAdd(&p.tally[1], acc_changed);
