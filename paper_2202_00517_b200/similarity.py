@@ -17,6 +17,8 @@ bit-identical numpy draws.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -60,6 +62,32 @@ def _stream(device: torch.device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
+_STAGE_MIN = 16 << 20  # bytes; below this a plain pageable copy is as fast
+
+
+def upload(host: np.ndarray, device: torch.device) -> torch.Tensor:
+    """Host array -> device tensor through pinned memory: the copy into the
+    (cached) pinned buffer is split over host threads (numpy releases the GIL),
+    then one DMA.  A pageable 160 MB copy runs at ~10 GB/s; this at several
+    times that."""
+    src = np.ascontiguousarray(host)
+    if src.nbytes < _STAGE_MIN or device.type != "cuda":
+        return torch.from_numpy(src).to(device)
+    from concurrent.futures import ThreadPoolExecutor
+
+    pinned = torch.empty(src.shape, dtype=torch.from_numpy(src[:0]).dtype, pin_memory=True)
+    dst = pinned.numpy().reshape(-1)
+    flat = src.reshape(-1)
+    parts = min(8, max(1, (os.cpu_count() or 1)))
+    bounds = np.linspace(0, flat.size, parts + 1, dtype=np.int64)
+    with ThreadPoolExecutor(max_workers=parts) as pool:
+        list(pool.map(lambda i: np.copyto(dst[bounds[i]:bounds[i + 1]], flat[bounds[i]:bounds[i + 1]]),
+                      range(parts)))
+    out = pinned.to(device, non_blocking=True)
+    torch.cuda.current_stream(device).synchronize()  # `pinned` returns to torch's cache only when unused
+    return out
+
+
 def _dev(device) -> torch.device:
     if device is None and not torch.cuda.is_available():
         raise RuntimeError("no CUDA device: the B200 KL local join has no CPU fallback")
@@ -76,18 +104,16 @@ class DeviceTables:
 
     kind = "kl"
 
-    def __init__(self, points: np.ndarray, device: torch.device, pinned: bool = False):
+    def __init__(self, points: np.ndarray, device: torch.device):
         self.device = device
         self.n, self.d = points.shape
         self.ld = (self.d + 3) // 4 * 4
-        host = torch.from_numpy(np.ascontiguousarray(points, dtype=np.float64))
-        if pinned:
-            host = host.pin_memory()
-        self.points = host.to(device, non_blocking=True)
+        host = np.ascontiguousarray(points, dtype=np.float64)
+        self.points = upload(host, device)
         self.log32 = torch.empty((self.n, self.ld), dtype=torch.float32, device=device)
         self.log64 = torch.empty((self.n, self.d), dtype=torch.float64, device=device)
         self.xlogx = torch.empty((self.n,), dtype=torch.float64, device=device)
-        self.h2d_bytes = host.numel() * 8
+        self.h2d_bytes = host.size * 8
         # all coordinates <= 1 -> all logs <= 0 (lets the join skip one accumulator)
         self.max_coord = float(self.points.max().item()) if points.size else 0.0
         _lib.call("knnd_kl_prepare", self.points.data_ptr(), self.n, self.d, self.ld, self.log32.data_ptr(),
@@ -134,7 +160,7 @@ class L2Tables:
         self.n, self.d = vectors.shape
         self.ld = (self.d + 1 + 3) // 4 * 4  # room for the squared norm column
         self.dplan = self.d + 1
-        v = torch.from_numpy(np.ascontiguousarray(vectors, dtype=np.float64)).to(device)
+        v = upload(np.ascontiguousarray(vectors, dtype=np.float64), device)
         sq_d = torch.from_numpy(np.ascontiguousarray(sq, dtype=np.float64)).to(device)
         center = torch.from_numpy(np.ascontiguousarray(vectors.mean(axis=0), dtype=np.float64)).to(device)
         self.rows64 = torch.empty((self.n, self.d + 1), dtype=torch.float64, device=device)
