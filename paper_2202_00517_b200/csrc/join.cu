@@ -582,7 +582,8 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     }
     __syncthreads();
 
-    // ---- phase 1: pre-dedup enumeration + hash dedup
+    // ---- phase 1: pre-dedup enumeration + hash dedup (one list atomic per warp
+    // and group of UNR1 ids per thread)
     {
       int s = s_init, j = j_init;
       const int iters = (total + G - 1) / G;
@@ -603,12 +604,26 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
             ++s;
           }
         }
+        bool nw[UNR1];
+#pragma unroll
+        for (int u = 0; u < UNR1; ++u)
+          nw[u] = id[u] >= 0 && id[u] != x && hash_insert_cas(table, id[u], shift, (unsigned)H - 1u);
+        unsigned m[UNR1];
+        int tot = 0;
 #pragma unroll
         for (int u = 0; u < UNR1; ++u) {
-          const int y = id[u];
-          bool isnew = false;
-          if (y >= 0 && y != x) isnew = hash_insert_cas(table, y, shift, (unsigned)H - 1u);
-          warp_append(isnew, y, &hdr[0], list, lane);
+          m[u] = __ballot_sync(FULL, nw[u]);
+          tot += __popc(m[u]);
+        }
+        if (tot) {
+          int b0 = 0;
+          if (lane == 0) b0 = atomicAdd(&hdr[0], tot);
+          b0 = __shfl_sync(FULL, b0, 0);
+#pragma unroll
+          for (int u = 0; u < UNR1; ++u) {
+            if (nw[u]) list[b0 + __popc(m[u] & lanemask_lt())] = id[u];
+            b0 += __popc(m[u]);
+          }
         }
       }
     }
