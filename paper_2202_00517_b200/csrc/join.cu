@@ -77,8 +77,11 @@ __host__ __device__ inline size_t al16(size_t v) { return (v + 15) & ~(size_t)15
 
 __device__ __forceinline__ unsigned hash_slot(int y, unsigned shift) { return ((unsigned)y * 0x9E3779B1u) >> shift; }
 
-// block-wide insert (several warps share the table): 4-slot buckets, one int4
-// read finds a duplicate without atomics; new ids CAS the first empty slot
+// Insert into 4-slot buckets (one int4 read finds a duplicate without atomics;
+// a new id CAS-es the first empty slot).  Buckets fill left to right — a CAS
+// only ever targets the first slot its reader saw empty, and slots are never
+// freed — so the first empty slot is the number of occupied ones (ids >= 0,
+// EMPTY = -1: count the sign bits) and a bucket is full iff its last slot is.
 __device__ __forceinline__ bool hash_insert_cas(int32_t *table, int y, unsigned shift, unsigned mask) {
   const unsigned bmask = mask >> 2;
   unsigned b = hash_slot(y, shift + 2);
@@ -86,9 +89,9 @@ __device__ __forceinline__ bool hash_insert_cas(int32_t *table, int y, unsigned 
     asm volatile("" ::: "memory");  // re-read the bucket every pass (other warps insert concurrently)
     const int4 v = reinterpret_cast<const int4 *>(table)[b];
     if ((v.x == y) | (v.y == y) | (v.z == y) | (v.w == y)) return false;
-    const unsigned emp = (v.x == EMPTY) | ((v.y == EMPTY) << 1) | ((v.z == EMPTY) << 2) | ((v.w == EMPTY) << 3);
-    if (emp) {
-      const int prev = atomicCAS(table + b * 4 + (__ffs(emp) - 1), EMPTY, y);
+    if (v.w == EMPTY) {
+      const int occ = 4 + (v.x >> 31) + (v.y >> 31) + (v.z >> 31) + (v.w >> 31);
+      const int prev = atomicCAS(table + b * 4 + occ, EMPTY, y);
       if (prev == EMPTY) return true;
       if (prev == y) return false;
       continue;  // lost the slot to another id: re-read the bucket
