@@ -10,8 +10,9 @@ initial row sort and FCC statistic in hand-written sm_100a kernels
 The exact K-NN ground truth and recall (evaluation.py:36-137) run on the GPU
 too (knnd_exact_knn).  The KL and squared-Euclidean ranking systems
 (similarity.py:80-140) are accelerated through the same fused join; other
-ranking systems, the metrizability checker, the bench harness and the CLI are
-out of scope.
+ranking systems, the metrizability checker and the CLI are out of scope (see
+DESIGN.md).  ``paper_2202_00517_b200.bench`` mirrors the reference's experiment
+harness (run_experiment / dimension_sweep / emit_report / emit_sweep).
 """
 
 from ._lib import EXPORTS, KnndError, launch_count
@@ -36,7 +37,7 @@ from .descent import (
     run_round,
     run_to_fixed_point,
 )
-from . import evaluation
+from . import bench, evaluation
 from .evaluation import ExactKnnGraph, exact_knn, exact_rows, recall, sampled_recall, uniform_recall_sample
 from .similarity import (
     EuclideanRankingSystem,
@@ -68,6 +69,7 @@ __all__ = [
     "ScoredRankingSystem",
     "derive_rng",
     "euclidean_ranking",
+    "bench",
     "evaluation",
     "exact_knn",
     "exact_rows",
