@@ -106,6 +106,7 @@ int knnd_csr_build(const int32_t *friends, int64_t n, int32_t k, int64_t row_lo,
  * Results do not depend on flags (only the work does).
  */
 #define KNND_JOIN_NONPOS_LOG 1u
+#define KNND_MAX_PEERS 15
 size_t knnd_local_join_workspace_bytes(int64_t n, int32_t d, int32_t k, int64_t row_lo,
                                        int64_t row_hi, int32_t max_indeg);
 int knnd_local_join(const double *points, const float *log32, const double *log64,
@@ -115,6 +116,29 @@ int knnd_local_join(const double *points, const float *log32, const double *log6
                     int32_t max_indeg, int32_t *out_ids, double *out_kl,
                     int32_t *out_ucount, unsigned long long *tally, const float *bound_in,
                     float *bound_out, void *ws, size_t ws_bytes, uint32_t flags, void *stream);
+
+/*
+ * The local join fused with the table exchange of a row-sharded round
+ * (run_round's snapshot semantics, descent.py:282-314, over P ranks; the
+ * reference has one process, so this replaces the all-gather the sharded
+ * engine would otherwise need after every join).  Identical to
+ * knnd_local_join, plus: each row written to out_ids (row x - row_lo of this
+ * rank's slice) is also stored at row x of every table in peer_tables[0..npeers)
+ * — host array of device pointers to row 0 of the other ranks' (n, k) next
+ * tables, mapped into this device's address space (CUDA IPC / symmetric
+ * memory over NVLink).  The stores overlap the join; before any rank reads the
+ * gathered table, the caller runs a cross-rank barrier on the stream (the
+ * kernels end with a system-scope fence).  npeers in 0..KNND_MAX_PEERS.
+ */
+int knnd_local_join_peers(const double *points, const float *log32, const double *log64,
+                          const double *xlogx, int64_t n, int32_t d, int32_t ld32,
+                          const int32_t *friends, int32_t k, const int64_t *indptr,
+                          const int32_t *indices, int64_t row_lo, int64_t row_hi,
+                          int32_t max_indeg, int32_t *out_ids, double *out_kl,
+                          int32_t *out_ucount, unsigned long long *tally,
+                          const float *bound_in, float *bound_out, void *ws, size_t ws_bytes,
+                          uint32_t flags, int32_t *const *peer_tables, int32_t npeers,
+                          void *stream);
 
 /*
  * Friend clustering rate count — friend_clustering_rate (descent.py:317-338)
@@ -203,6 +227,15 @@ int knnd_l2_local_join(const float *anchor32, const float *cand32, const double 
                        int32_t *out_ids, double *out_d2, int32_t *out_ucount,
                        unsigned long long *tally, const float *bound_in, float *bound_out, void *ws,
                        size_t ws_bytes, void *stream);
+/* knnd_l2_local_join with the fused table exchange of knnd_local_join_peers */
+int knnd_l2_local_join_peers(const float *anchor32, const float *cand32, const double *rows64,
+                             const double *sq64, int64_t n, int32_t d, int32_t ld32,
+                             double maxnorm, const int32_t *friends, int32_t k,
+                             const int64_t *indptr, const int32_t *indices, int64_t row_lo,
+                             int64_t row_hi, int32_t max_indeg, int32_t *out_ids, double *out_d2,
+                             int32_t *out_ucount, unsigned long long *tally,
+                             const float *bound_in, float *bound_out, void *ws, size_t ws_bytes,
+                             int32_t *const *peer_tables, int32_t npeers, void *stream);
 int knnd_l2_exact_knn(const float *anchor32, const float *cand32, const double *rows64,
                       const double *sq64, int64_t n, int32_t d, int32_t ld32, double maxnorm,
                       const int32_t *queries, int64_t nq, int32_t k, int32_t cap, int32_t *out_ids,

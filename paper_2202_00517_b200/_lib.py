@@ -37,6 +37,8 @@ _SIGS = {
     "knnd_local_join_workspace_bytes": ([_I64, _I32, _I32, _I64, _I64, _I32], _SZ),
     "knnd_local_join": ([_P, _P, _P, _P, _I64, _I32, _I32, _P, _I32, _P, _P, _I64, _I64, _I32, _P, _P, _P, _P,
                          _P, _P, _P, _SZ, C.c_uint32, _P], C.c_int),
+    "knnd_local_join_peers": ([_P, _P, _P, _P, _I64, _I32, _I32, _P, _I32, _P, _P, _I64, _I64, _I32, _P, _P, _P,
+                               _P, _P, _P, _P, _SZ, C.c_uint32, _P, _I32, _P], C.c_int),
     "knnd_fcc": ([_P, _I64, _I32, _P, _P, _P, _I32, _P, _P], C.c_int),
     "knnd_sort_rows": ([_P, _P, _P, _I64, _I32, _I32, _I64, _I64, _P, _P, _P, _P], C.c_int),
     "knnd_exact_knn_workspace_bytes": ([_I64, _I32], _SZ),
@@ -47,6 +49,8 @@ _SIGS = {
     "knnd_l2_sort_rows": ([_P, _P, _I64, _I32, _I32, _I64, _I64, _P, _P, _P, _P], C.c_int),
     "knnd_l2_local_join": ([_P, _P, _P, _P, _I64, _I32, _I32, C.c_double, _P, _I32, _P, _P, _I64, _I64, _I32, _P, _P,
                             _P, _P, _P, _P, _P, _SZ, _P], C.c_int),
+    "knnd_l2_local_join_peers": ([_P, _P, _P, _P, _I64, _I32, _I32, C.c_double, _P, _I32, _P, _P, _I64, _I64, _I32,
+                                  _P, _P, _P, _P, _P, _P, _P, _SZ, _P, _I32, _P], C.c_int),
     "knnd_l2_exact_knn": ([_P, _P, _P, _P, _I64, _I32, _I32, C.c_double, _P, _I64, _I32, _I32, _P, _P, _P, _P, _SZ,
                            _P], C.c_int),
     "knnd_random_kout_workspace_bytes": ([_I64, _I32], _SZ),
@@ -57,6 +61,14 @@ _SIGS = {
 EXPORTS = tuple(_SIGS)
 
 JOIN_NONPOS_LOG = 1  # KNND_JOIN_NONPOS_LOG
+MAX_PEERS = 15  # KNND_MAX_PEERS
+
+
+def peer_array(ptrs) -> C.Array | None:
+    """Host array of peer-table device pointers for the *_local_join_peers entries."""
+    if not ptrs:
+        return None
+    return (C.c_void_p * len(ptrs))(*[int(x) for x in ptrs])
 
 
 def load(path: str | None = None):

@@ -68,7 +68,17 @@ struct JoinParams {
   // relative and inside `band`; L2: (d+4) 2^-53 (2 maxnorm)^2 >= |fl(d2) - d2|);
   // the screen band of an anchor is 2 (band * am + slack)
   float slack;
+  // fused table exchange (knnd_local_join_peers): every written row is also
+  // stored at row x of each peer's next table (NVLink peer memory), so the
+  // rows reach the other ranks while the join runs — no all-gather afterwards
+  int npeers;
+  int32_t *peers[KNND_MAX_PEERS];
 };
+
+// the row's K ids to every peer table (row x, absolute) — lane i stores id i
+__device__ __forceinline__ void store_peers(const JoinParams &p, int64_t x, int i, int id) {
+  for (int q = 0; q < p.npeers; ++q) p.peers[q][x * p.K + i] = id;
+}
 
 __host__ __device__ inline size_t al16(size_t v) { return (v + 15) & ~(size_t)15; }
 
@@ -276,6 +286,7 @@ __device__ __forceinline__ bool emit_row(const JoinParams &p, const WarpTopK<Key
     if (i < K) {
       const KeyD kq = ex.b[q];
       p.out_ids[xr * K + i] = kq.id;
+      store_peers(p, x, i, kq.id);
       if (p.out_kl) p.out_kl[xr * K + i] = kq.s;
       diff |= kq.id != __ldg(p.F + (int64_t)x * K + i);
     }
@@ -354,6 +365,7 @@ __device__ __forceinline__ bool certify_row(const JoinParams &p, const int32_t *
   bool d = false;
   if (lane < K) {
     p.out_ids[xr * K + lane] = key.id();
+    store_peers(p, x, lane, key.id());
     d = key.id() != __ldg(p.F + (int64_t)x * K + lane);
   }
   diff = __any_sync(FULL, d);
@@ -841,6 +853,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     pb ^= 1;
   }
   cp_async_wait_all();
+  if (p.npeers) __threadfence_system();  // peer rows performed before the caller's cross-rank barrier
   if (tid == 0) {
     if (acc_comp) atomicAdd(&p.tally[0], acc_comp);
     if (acc_changed) atomicAdd(&p.tally[1], acc_changed);
@@ -1186,6 +1199,7 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
     pb ^= 1;
   }
   cp_async_wait_all();
+  if (p.npeers) __threadfence_system();  // peer rows performed before the caller's cross-rank barrier
   if (lane == 0) {
     if (acc_comp) atomicAdd(&p.tally[0], acc_comp);
     if (acc_changed) atomicAdd(&p.tally[1], acc_changed);
@@ -1560,13 +1574,28 @@ static int join_run(const char *who, JoinParams &p, int64_t n, int32_t dplan, in
   return KNND_OK;
 }
 
+// peer tables of the fused exchange (host array of device pointers)
+static int set_peers(JoinParams &p, const char *who, int32_t *const *peer_tables, int32_t npeers) {
+  KNND_CHECK_ARG(npeers >= 0 && npeers <= KNND_MAX_PEERS, "%s: npeers=%d outside 0..%d", who, npeers,
+                 KNND_MAX_PEERS);
+  KNND_CHECK_ARG(npeers == 0 || peer_tables, "%s: null peer_tables", who);
+  p.npeers = npeers;
+  for (int q = 0; q < npeers; ++q) {
+    KNND_CHECK_ARG(peer_tables[q], "%s: null peer table %d", who, q);
+    p.peers[q] = peer_tables[q];
+  }
+  return KNND_OK;
+}
+
 extern "C" {
 
-int knnd_local_join(const double *points, const float *log32, const double *log64, const double *xlogx, int64_t n,
-                    int32_t d, int32_t ld32, const int32_t *friends, int32_t k, const int64_t *indptr,
-                    const int32_t *indices, int64_t row_lo, int64_t row_hi, int32_t max_indeg, int32_t *out_ids,
-                    double *out_kl, int32_t *out_ucount, unsigned long long *tally, const float *bound_in,
-                    float *bound_out, void *ws, size_t ws_bytes, uint32_t flags, void *stream) {
+int knnd_local_join_peers(const double *points, const float *log32, const double *log64, const double *xlogx,
+                          int64_t n, int32_t d, int32_t ld32, const int32_t *friends, int32_t k,
+                          const int64_t *indptr, const int32_t *indices, int64_t row_lo, int64_t row_hi,
+                          int32_t max_indeg, int32_t *out_ids, double *out_kl, int32_t *out_ucount,
+                          unsigned long long *tally, const float *bound_in, float *bound_out, void *ws,
+                          size_t ws_bytes, uint32_t flags, int32_t *const *peer_tables, int32_t npeers,
+                          void *stream) {
   KNND_CHECK_ARG(points && log32 && log64 && xlogx, "knnd_local_join: null pointer");
   JoinParams p{};
   p.points = points;
@@ -1589,15 +1618,26 @@ int knnd_local_join(const double *points, const float *log32, const double *log6
   p.d64 = d;
   p.pstride = d;
   p.aside32 = nullptr;
+  if (int rc = set_peers(p, "knnd_local_join", peer_tables, npeers)) return rc;
   return join_run("knnd_local_join", p, n, d, k, row_lo, row_hi, max_indeg, ws, ws_bytes, stream);
 }
 
-int knnd_l2_local_join(const float *anchor32, const float *cand32, const double *rows64, const double *sq64,
-                       int64_t n, int32_t d, int32_t ld32, double maxnorm, const int32_t *friends, int32_t k,
-                       const int64_t *indptr, const int32_t *indices, int64_t row_lo, int64_t row_hi,
-                       int32_t max_indeg, int32_t *out_ids, double *out_d2, int32_t *out_ucount,
-                       unsigned long long *tally, const float *bound_in, float *bound_out, void *ws, size_t ws_bytes,
-                       void *stream) {
+int knnd_local_join(const double *points, const float *log32, const double *log64, const double *xlogx, int64_t n,
+                    int32_t d, int32_t ld32, const int32_t *friends, int32_t k, const int64_t *indptr,
+                    const int32_t *indices, int64_t row_lo, int64_t row_hi, int32_t max_indeg, int32_t *out_ids,
+                    double *out_kl, int32_t *out_ucount, unsigned long long *tally, const float *bound_in,
+                    float *bound_out, void *ws, size_t ws_bytes, uint32_t flags, void *stream) {
+  return knnd_local_join_peers(points, log32, log64, xlogx, n, d, ld32, friends, k, indptr, indices, row_lo, row_hi,
+                               max_indeg, out_ids, out_kl, out_ucount, tally, bound_in, bound_out, ws, ws_bytes, flags,
+                               nullptr, 0, stream);
+}
+
+int knnd_l2_local_join_peers(const float *anchor32, const float *cand32, const double *rows64, const double *sq64,
+                             int64_t n, int32_t d, int32_t ld32, double maxnorm, const int32_t *friends, int32_t k,
+                             const int64_t *indptr, const int32_t *indices, int64_t row_lo, int64_t row_hi,
+                             int32_t max_indeg, int32_t *out_ids, double *out_d2, int32_t *out_ucount,
+                             unsigned long long *tally, const float *bound_in, float *bound_out, void *ws,
+                             size_t ws_bytes, int32_t *const *peer_tables, int32_t npeers, void *stream) {
   KNND_CHECK_ARG(anchor32 && cand32 && rows64 && sq64, "knnd_l2_local_join: null pointer");
   JoinParams p{};
   p.points = rows64;  // the anchor's fp64 coordinates: the first d entries of its row
@@ -1621,7 +1661,19 @@ int knnd_l2_local_join(const float *anchor32, const float *cand32, const double 
   p.pstride = d + 1;
   p.aside32 = anchor32;
   p.slack = (float)((d + 4) * 0x1p-53 * 4.0 * maxnorm * maxnorm);
+  if (int rc = set_peers(p, "knnd_l2_local_join", peer_tables, npeers)) return rc;
   return join_run("knnd_l2_local_join", p, n, d + 1, k, row_lo, row_hi, max_indeg, ws, ws_bytes, stream);
+}
+
+int knnd_l2_local_join(const float *anchor32, const float *cand32, const double *rows64, const double *sq64,
+                       int64_t n, int32_t d, int32_t ld32, double maxnorm, const int32_t *friends, int32_t k,
+                       const int64_t *indptr, const int32_t *indices, int64_t row_lo, int64_t row_hi,
+                       int32_t max_indeg, int32_t *out_ids, double *out_d2, int32_t *out_ucount,
+                       unsigned long long *tally, const float *bound_in, float *bound_out, void *ws, size_t ws_bytes,
+                       void *stream) {
+  return knnd_l2_local_join_peers(anchor32, cand32, rows64, sq64, n, d, ld32, maxnorm, friends, k, indptr, indices,
+                                  row_lo, row_hi, max_indeg, out_ids, out_d2, out_ucount, tally, bound_in, bound_out,
+                                  ws, ws_bytes, nullptr, 0, stream);
 }
 
 }  // extern "C"

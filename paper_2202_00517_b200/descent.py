@@ -414,6 +414,8 @@ def descend_resident(eng: Engine, tabs, table: torch.Tensor, samples_dev: torch.
     Sorts the initial rows (K6), then runs rounds until the FCC stalls (or no
     row changes).  Returns (final KnnState, [RoundStats])."""
     s = eng.shard
+    if s.world > 1:
+        eng.enable_peer_exchange()  # fused join + table exchange when the ranks can map each other
     eng.ops.sort_rows(tabs, eng.own_rows(table), eng.k, s.lo, s.hi)
     eng.exchange(table)
     csr, mx = eng.build_csr(table)

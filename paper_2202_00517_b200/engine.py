@@ -7,10 +7,17 @@ int32 friends table (padded to P*chunk rows so the NCCL all-gather is
 in-place and equal-sized).  A round (run_round, descent.py:282-314) is:
 
   local join (own anchors -> own slice of the next table)     knnd_local_join
-  all-gather of the next table, all-reduce of the tallies      NCCL (P > 1)
+  exchange of the next table, all-reduce of the tallies        (P > 1, below)
   co-friend CSR of the next table for own targets              knnd_csr_build
   FCC count of the next table (replicated on every rank)       knnd_fcc
   one small device->host read: tallies, FCC count, max in-degree
+
+The exchange (P > 1) is fused into the join by default: the next tables are a
+ping-pong pair in symmetric memory (every rank maps every rank's copy over
+NVLink), and the join kernel stores each finished row into every peer's copy
+as it goes (knnd_local_join_peers) — the transfer overlaps the join, and a
+device-side cross-rank barrier replaces the all-gather.  KNND_EXCHANGE=nccl
+selects the plain in-place NCCL all-gather after the join instead.
 
 The kernel calls go through an ``ops`` object; ``CudaOps`` is the product
 (libknnd.so).  Tests inject a CPU stand-in to exercise the multi-rank logic
@@ -19,7 +26,10 @@ under the gloo backend without a GPU.
 
 from __future__ import annotations
 
+import os
+import sys
 from dataclasses import dataclass
+from typing import Callable
 
 import numpy as np
 import torch
@@ -88,14 +98,16 @@ class CudaOps:
     def join(self, tabs, table: torch.Tensor, n: int, k: int, csr: Csr, max_indeg: int, out_rows: torch.Tensor,
              tally: torch.Tensor, out_kl: torch.Tensor | None = None, out_ucount: torch.Tensor | None = None,
              flags: int | None = None, bound_in: torch.Tensor | None = None,
-             bound_out: torch.Tensor | None = None) -> None:
-        """knnd_local_join (KL) / knnd_l2_local_join (Euclidean), by the tables' metric."""
+             bound_out: torch.Tensor | None = None, peers=()) -> None:
+        """knnd_local_join_peers (KL) / knnd_l2_local_join_peers (Euclidean), by
+        the tables' metric; `peers` = device addresses of the other ranks'
+        next tables (row 0), or empty."""
         if flags is None:
             flags = tabs.join_flags()
         nbytes = _lib.load().knnd_local_join_workspace_bytes(n, tabs.dplan, k, csr.lo, csr.hi, max_indeg)
         ws = self._workspace("join", nbytes)
         tabs.join(table, k, csr, max_indeg, out_rows, tally, out_kl, out_ucount, bound_in, bound_out, ws, flags,
-                  self._stream())
+                  self._stream(), peers=tuple(peers))
 
     def random_kout(self, state: tuple, n: int, k: int, table: torch.Tensor, out_meta: torch.Tensor,
                     bad: torch.Tensor) -> None:
@@ -117,6 +129,54 @@ class CudaOps:
     def sort_rows(self, tabs, rows: torch.Tensor, k: int, lo: int, hi: int, out_kl: torch.Tensor | None = None):
         # in place: each warp reads its row before writing it back
         tabs.sort_rows(rows, k, lo, hi, out_kl, self._stream())
+
+
+class PeerTables:
+    """The ping-pong pair of next tables of the fused exchange.
+
+    bufs[i]   this rank's copy of table i, (padded_rows, K) int32
+    peers[i]  the other ranks' copies of table i as this process addresses
+              them (device pointers for CudaOps; tensors for the CPU stand-in)
+    barrier(i) a cross-rank barrier on the current stream after which every
+              copy of table i holds every rank's rows
+
+    Round r reads one table and writes the other on every rank, so a copy is
+    only overwritten after every rank has passed the barrier of the round that
+    last read it.  A table returned in a KnnState stays valid until the round
+    after next (descend_resident only hands out the final one)."""
+
+    def __init__(self, bufs: list, peers: list, barrier: Callable[[int], None]):
+        self.bufs, self.peers, self.barrier = bufs, peers, barrier
+
+    def pick(self, table: torch.Tensor) -> int:
+        """Index of the table the round reading `table` writes."""
+        return 1 if table.data_ptr() == self.bufs[0].data_ptr() else 0
+
+
+def symmetric_peer_tables(eng: "Engine") -> PeerTables:
+    """Both tables in torch symmetric memory (CUDA IPC mappings of every rank's
+    buffer over NVLink), rendezvoused once per engine."""
+    import torch.distributed._symmetric_memory as symm
+
+    group = eng.group if eng.group is not None else dist.group.WORLD
+    bufs, handles = [], []
+    for _ in range(2):
+        t = symm.empty((eng.shard.padded_rows, eng.k), dtype=torch.int32, device=eng.device)
+        handles.append(symm.rendezvous(t, group))
+        bufs.append(t)
+    me, world = eng.shard.rank, eng.shard.world
+    peers = [[int(h.buffer_ptrs[r]) for r in range(world) if r != me] for h in handles]
+    return PeerTables(bufs, peers, lambda i: handles[i].barrier(channel=0))
+
+
+def exchange_mode(eng: "Engine") -> str:
+    """'peer' (fused stores, default for P > 1 on CUDA + NCCL) or 'nccl'."""
+    want = os.environ.get("KNND_EXCHANGE", "peer")
+    if want not in ("peer", "nccl"):
+        raise ValueError(f"KNND_EXCHANGE must be 'peer' or 'nccl', got {want!r}")
+    if eng.shard.world == 1 or eng.device.type != "cuda" or dist.get_backend(eng.group) != "nccl":
+        return "nccl"
+    return want
 
 
 @dataclass
@@ -149,6 +209,21 @@ class Engine:
         self._stats32 = self.stats.view(torch.int32)
         # optional CUDA-event bracketing of each local join (bench.py roofline)
         self.join_events: list | None = None
+        self.peer: PeerTables | None = None  # fused exchange (P > 1), see enable_peer_exchange
+
+    def enable_peer_exchange(self, peer: PeerTables | None = None) -> bool:
+        """Switch rounds to the fused exchange (idempotent).  Without an explicit
+        `peer`, maps symmetric-memory tables when exchange_mode() says so; if
+        that mapping fails the engine keeps the NCCL all-gather and says why."""
+        if peer is not None:
+            self.peer = peer
+        elif self.peer is None and exchange_mode(self) == "peer":
+            try:
+                self.peer = symmetric_peer_tables(self)
+            except Exception as exc:  # e.g. no P2P / IPC between these devices
+                print(f"knnd: fused peer exchange unavailable ({type(exc).__name__}: {exc}); "
+                      "using the NCCL all-gather", file=sys.stderr)
+        return self.peer is not None
 
     # -- tables -----------------------------------------------------------
     def alloc_table(self) -> torch.Tensor:
@@ -210,7 +285,11 @@ class Engine:
         `table` with the same `tabs` (or None); the new one is returned."""
         tally = self.stats[0:4]
         tally.zero_()
-        nxt = self.alloc_table()
+        if self.peer is not None:
+            ip = self.peer.pick(table)
+            nxt, peers = self.peer.bufs[ip], self.peer.peers[ip]
+        else:
+            nxt, peers = self.alloc_table(), ()
         s = self.shard
         bound_out = torch.empty(max(s.hi - s.lo, 1), dtype=torch.float32, device=self.device)
         ev = None
@@ -218,12 +297,15 @@ class Engine:
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             ev[0].record()
         self.ops.join(tabs, table, self.n, self.k, csr, max_indeg, self.own_rows(nxt), tally, out_kl, out_ucount,
-                      bound_in=bound, bound_out=bound_out)
+                      bound_in=bound, bound_out=bound_out, peers=peers)
         if ev is not None:
             ev[1].record()
         self.stats[5:6].copy_(tally[0:1])  # this rank's comparisons (before the all-reduce)
         if self.shard.world > 1:
-            self.exchange(nxt)
+            if self.peer is not None:
+                self.peer.barrier(ip)  # every rank's rows are in every copy
+            else:
+                self.exchange(nxt)
             dist.all_reduce(tally, group=self.group)
         csr_next = self.ops.csr(nxt, self.n, self.k, s.lo, s.hi, self._stats32[9:10])
         if samples is not None:

@@ -122,12 +122,12 @@ class DeviceTables:
 
     # -- the kernel calls (one per ABI entry; the L2 tables provide the same methods)
     def join(self, table, k, csr, max_indeg, out_rows, tally, out_scores, out_ucount, bound_in, bound_out, ws,
-             flags, stream):
-        _lib.call("knnd_local_join", self.points.data_ptr(), self.log32.data_ptr(), self.log64.data_ptr(),
+             flags, stream, peers=()):
+        _lib.call("knnd_local_join_peers", self.points.data_ptr(), self.log32.data_ptr(), self.log64.data_ptr(),
                   self.xlogx.data_ptr(), self.n, self.d, self.ld, table.data_ptr(), k, csr.indptr.data_ptr(),
                   csr.indices.data_ptr(), csr.lo, csr.hi, max_indeg, out_rows.data_ptr(), _ptr(out_scores),
                   _ptr(out_ucount), tally.data_ptr(), _ptr(bound_in), _ptr(bound_out), ws.data_ptr(), ws.numel(),
-                  flags, stream)
+                  flags, _lib.peer_array(peers), len(peers), stream)
 
     def join_flags(self) -> int:
         return _lib.JOIN_NONPOS_LOG if self.max_coord <= 1.0 else 0
@@ -174,12 +174,12 @@ class L2Tables:
         torch.cuda.current_stream(device).synchronize()  # v and center are temporaries
 
     def join(self, table, k, csr, max_indeg, out_rows, tally, out_scores, out_ucount, bound_in, bound_out, ws,
-             flags, stream):
-        _lib.call("knnd_l2_local_join", self.anchor32.data_ptr(), self.cand32.data_ptr(), self.rows64.data_ptr(),
-                  self.sq64.data_ptr(), self.n, self.d, self.ld, self.maxnorm, table.data_ptr(), k,
-                  csr.indptr.data_ptr(), csr.indices.data_ptr(), csr.lo, csr.hi, max_indeg, out_rows.data_ptr(),
-                  _ptr(out_scores), _ptr(out_ucount), tally.data_ptr(), _ptr(bound_in), _ptr(bound_out),
-                  ws.data_ptr(), ws.numel(), stream)
+             flags, stream, peers=()):
+        _lib.call("knnd_l2_local_join_peers", self.anchor32.data_ptr(), self.cand32.data_ptr(),
+                  self.rows64.data_ptr(), self.sq64.data_ptr(), self.n, self.d, self.ld, self.maxnorm,
+                  table.data_ptr(), k, csr.indptr.data_ptr(), csr.indices.data_ptr(), csr.lo, csr.hi, max_indeg,
+                  out_rows.data_ptr(), _ptr(out_scores), _ptr(out_ucount), tally.data_ptr(), _ptr(bound_in),
+                  _ptr(bound_out), ws.data_ptr(), ws.numel(), _lib.peer_array(peers), len(peers), stream)
 
     def join_flags(self) -> int:
         return 0

@@ -21,7 +21,7 @@ class CpuOps:
         return Csr(torch.from_numpy(sub_ptr.copy()), torch.from_numpy(sub_idx), lo, hi)
 
     def join(self, tabs, table, n, k, csr, max_indeg, out_rows, tally, out_kl=None, out_ucount=None, flags=None,
-             bound_in=None, bound_out=None):
+             bound_in=None, bound_out=None, peers=()):
         if bound_out is not None:
             bound_out.fill_(float("nan"))  # no bound: the device kernel treats NaN as unknown
         full_ptr = np.zeros(n + 1, np.int64)
@@ -29,6 +29,8 @@ class CpuOps:
         rows, kl, uc, comps, changed = native.local_join(tabs, table[:n].numpy(), np.arange(csr.lo, csr.hi),
                                                          csr=(full_ptr, csr.indices.numpy()))
         out_rows.copy_(torch.from_numpy(rows))
+        for t in peers:  # the fused exchange: this rank's rows into every peer's copy (shared memory here)
+            t[csr.lo:csr.hi].copy_(out_rows)
         tally[0] += comps
         tally[1] += changed
         if out_kl is not None:

@@ -23,7 +23,7 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, meta, out):
+def _worker(rank, world, port, meta, out, shared=None):
     import sys
 
     sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
@@ -46,20 +46,32 @@ def _worker(rank, world, port, meta, out):
         rounds = cfg.resolved_max_rounds(n)
         eng = Engine(n, k, torch.device("cpu"), ops=CpuOps())
         assert eng.shard.world == world and eng.shard.rank == rank
+        if shared is not None:  # fused exchange: every rank's ping-pong tables in shared memory
+            from paper_2202_00517_b200.engine import PeerTables
+
+            peers = [[shared[q][i] for q in range(world) if q != rank] for i in range(2)]
+            assert eng.enable_peer_exchange(PeerTables(shared[rank], peers, lambda i: dist.barrier()))
         table = eng.alloc_table()
         eng.upload_rows(b2.random_kout_draws(n, k, b2.derive_rng(seed, 2)), table)
         smp = torch.from_numpy(draw_fcc_schedule(n, k, cfg, rounds))
         state, hist = descend_resident(eng, tab, table, smp, cfg.fcc_sample_count, rounds)
+        if shared is not None:
+            assert state._table.data_ptr() in (shared[rank][0].data_ptr(), shared[rank][1].data_ptr())
         out[rank] = {"sha": sha_i32(state.friends),
                      "hist": [(h.comparisons, h.changed_friend_sets, h.fcc) for h in hist]}
     finally:
         dist.destroy_process_group()
 
 
-def _run(world, meta):
+def _run(world, meta, peer=False):
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), meta, out), nprocs=world, join=True)
+    shared = None
+    if peer:
+        rows = -(-meta["n"] // world) * world
+        shared = [[torch.full((rows, meta["k"]), -7, dtype=torch.int32).share_memory_() for _ in range(2)]
+                  for _ in range(world)]
+    mp.spawn(_worker, args=(world, _free_port(), meta, out, shared), nprocs=world, join=True)
     return dict(out)
 
 
@@ -67,6 +79,19 @@ def _run(world, meta):
 def test_sharded_rounds_match_reference(small_meta, world):
     meta = small_meta[NAME]
     res = _run(world, meta)
+    expect = [(r["comparisons"], r["changed"], r["fcc"]) for r in meta["rounds"]]
+    for rank in range(world):
+        assert res[rank]["hist"] == expect, rank
+        assert res[rank]["sha"] == meta["rounds"][-1]["sha"], rank
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fused_peer_exchange_matches_reference(small_meta, world):
+    """The fused exchange (engine.PeerTables, each rank's join storing its rows
+    into every peer's copy, a barrier instead of the all-gather) on shared-memory
+    tables: same trajectory and final table as the reference."""
+    meta = small_meta[NAME]
+    res = _run(world, meta, peer=True)
     expect = [(r["comparisons"], r["changed"], r["fcc"]) for r in meta["rounds"]]
     for rank in range(world):
         assert res[rank]["hist"] == expect, rank
