@@ -33,7 +33,7 @@ import torch
 
 from .core import ConfigError, Dataset, ItemId
 from .engine import Csr, Engine
-from .similarity import device_tables_for
+from .similarity import device_for, device_tables_for
 
 _SEED_MASK = 0xFFFFFFFFFFFFFFFF
 
@@ -274,14 +274,27 @@ def device_random_kout(eng: Engine, n: int, k: int, rng: np.random.Generator, ta
     the rejection redraws of rows with duplicates run on the host, exactly as
     the reference does them.  Returns False (nothing done) when the generator is
     not PCG64 or the ops have no device path."""
+    finish = device_random_kout_async(eng, n, k, rng, table)
+    return finish is not None and finish()
+
+
+def device_random_kout_async(eng: Engine, n: int, k: int, rng: np.random.Generator, table: torch.Tensor):
+    """device_random_kout split at its one synchronisation: launches the draw
+    kernel and returns a `finish()` that completes the generator bookkeeping
+    and the duplicate-row redraws (returns True), or None when there is no
+    device path.  `rng` must not be used in between."""
     st = rng.bit_generator.state
     if st.get("bit_generator") != "PCG64" or not hasattr(eng.ops, "random_kout") or n - 1 > 0xFFFFFFFF:
-        return False
+        return None
     s0, inc = int(st["state"]["state"]), int(st["state"]["inc"])
     has, uint = int(st["has_uint32"]), int(st["uinteger"])
     meta = torch.zeros(2, dtype=torch.int64, device=eng.device)
     bad_dev = torch.empty(n, dtype=torch.int32, device=eng.device)
     eng.ops.random_kout((s0, inc, has, uint), n, k, table, meta, bad_dev)
+    return lambda: _finish_random_kout(eng, n, k, rng, table, meta, bad_dev, s0, inc, has)
+
+
+def _finish_random_kout(eng, n, k, rng, table, meta, bad_dev, s0, inc, has) -> bool:
     consumed, nbad = (int(v) for v in meta.cpu().tolist())  # nbad: an int32 in the low half of meta[1]
     fresh = consumed - has
     if has and fresh < 0:
@@ -440,13 +453,17 @@ def _run_rounds(dataset: Dataset, rs, cfg: DescentConfig, max_rounds: int, stop_
     k = cfg.k
     if n <= k:
         raise ConfigError(f"need n > k, got n={n}, k={k}")
-    tabs = device_tables_for(rs)
-    eng = Engine(n, k, tabs.device)
+    # the device draws, the host FCC schedule and the table upload overlap: the
+    # draw kernel runs while the host draws the schedule and stages the points
+    eng = Engine(n, k, device_for(rs))
     table = eng.alloc_table()
     rng = derive_rng(cfg.seed, STREAM_INIT)
-    if not (n - 1 > 2 * k * k and device_random_kout(eng, n, k, rng, table)):
+    finish = device_random_kout_async(eng, n, k, rng, table) if n - 1 > 2 * k * k else None
+    smp = draw_fcc_schedule(n, k, cfg, max_rounds)
+    tabs = device_tables_for(rs, eng.device)
+    if not (finish is not None and finish()):
         eng.upload_rows(random_kout_draws(n, k, rng), table)
-    smp_dev = _to_device(draw_fcc_schedule(n, k, cfg, max_rounds), tabs.device)
+    smp_dev = _to_device(smp, tabs.device)
     state, history = descend_resident(eng, tabs, table, smp_dev, cfg.fcc_sample_count, max_rounds,
                                       stop_on_fixed_point)
     return state.friends, history
