@@ -1236,7 +1236,8 @@ __global__ void classify_kernel(const int64_t *__restrict__ indptr, int64_t m, i
 // ---------------------------------------------------------------------------
 // host side: the size-class plan
 
-enum { KIND_WARP = 0, KIND_BLOCK128 = 1, KIND_BLOCK256 = 2, KIND_GLOBAL = 3, KIND_BLOCK64 = 4, KIND_WARPG = 5 };
+enum { KIND_WARP = 0, KIND_BLOCK128 = 1, KIND_BLOCK256 = 2, KIND_GLOBAL = 3, KIND_BLOCK64 = 4, KIND_WARPG = 5,
+       KIND_BLOCK512 = 6 };
 
 struct Cls {
   int kind, logH, sw;
@@ -1283,6 +1284,9 @@ static int parse_plan(const char *spec, int kind[], int logH[]) {
     } else if (q[0] == 'b' && !strncmp(q + 1, "256:", 4)) {
       k = KIND_BLOCK256;
       l = atoi(q + 5);
+    } else if (q[0] == 'b' && !strncmp(q + 1, "512:", 4)) {
+      k = KIND_BLOCK512;
+      l = atoi(q + 5);
     } else {
       return 0;
     }
@@ -1312,10 +1316,14 @@ static Plan make_plan(int64_t m, int d, int K, int max_indeg) {
   if (l1 < 9) l1 = 9;
   if (l1 > 12) l1 = 12;
   // measured on B200 at C3 (KNND_PLAN sweeps): warp / 128-thread blocks for two
-  // table sizes / 256-thread blocks up to 2^15 slots / global tables
+  // table sizes / 256-thread blocks for 2^14 slots / 512-thread blocks for 2^15
+  // (one block per SM there: the extra warps cut that class's time by 25%) /
+  // global tables
   int kind[MAXCLS] = {KIND_WARP, KIND_BLOCK128, KIND_BLOCK128, KIND_BLOCK256, KIND_BLOCK256};
   int logH[MAXCLS] = {l1, l1 + 1, l1 + 2, l1 + 3 < 15 ? l1 + 3 : 15, 15};
   int n = l1 + 3 < 15 ? 5 : 4;
+  for (int i = 0; i < n; ++i)
+    if (kind[i] == KIND_BLOCK256 && logH[i] == 15) kind[i] = KIND_BLOCK512;
   if (const char *env = getenv("KNND_PLAN")) {
     int k2[MAXCLS], l2[MAXCLS];
     const int n2 = parse_plan(env, k2, l2);
@@ -1469,6 +1477,8 @@ static int dispatch_class(const Plan &P, int i, const JoinParams &p, const int32
       return dispatch_block<128, false>(P, p, alist, acount, c.logH, c.sw, nullptr, 0, 0, st);
     case KIND_BLOCK256:
       return dispatch_block<256, false>(P, p, alist, acount, c.logH, c.sw, nullptr, 0, 0, st);
+    case KIND_BLOCK512:
+      return dispatch_block<512, false>(P, p, alist, acount, c.logH, c.sw, nullptr, 0, 0, st);
     default:
       return dispatch_block<GL, true>(P, p, alist, acount, c.logH, c.sw, slabs, P.slab_ints, P.nslab, st);
   }
