@@ -576,13 +576,24 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     int an = 0, xn = -1;
     int64_t nc0 = 0, nc1 = 0;
     if (tid == 0) an = atomicAdd(cursor, 1);  // used after phase 0 (latency off the path)
+    // global-memory tables are sized per anchor (>= 2P slots, at least 2^15): the
+    // slab fits the largest hub, but clearing and probing only what this anchor
+    // needs keeps the hub class from sweeping megabytes per anchor
+    int Ha = H;
+    unsigned sha = shift;
+    if constexpr (GTAB) {
+      int la = 15;
+      while (la < logH && (1 << la) < 2 * total) ++la;
+      Ha = 1 << la;
+      sha = 32u - (unsigned)la;
+    }
     cp_async_wait_all();
     __syncthreads();  // this anchor's inputs are in buffer pb; everyone has read hdr[8..12]
 
     // ---- phase 0: clear table + histograms (S and the anchor rows were prefetched)
     {
       int4 *t4 = reinterpret_cast<int4 *>(table);
-      for (int i = tid; i < (H >> 2); i += G) t4[i] = make_int4(EMPTY, EMPTY, EMPTY, EMPTY);
+      for (int i = tid; i < (Ha >> 2); i += G) t4[i] = make_int4(EMPTY, EMPTY, EMPTY, EMPTY);
     }
     for (int i = tid; i < 2 * NBIN; i += G) hist[i] = 0;
     if constexpr (GTAB)
@@ -622,7 +633,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
         bool nw[UNR1];
 #pragma unroll
         for (int u = 0; u < UNR1; ++u)
-          nw[u] = id[u] >= 0 && id[u] != x && hash_insert_cas(table, id[u], shift, (unsigned)H - 1u);
+          nw[u] = id[u] >= 0 && id[u] != x && hash_insert_cas(table, id[u], sha, (unsigned)Ha - 1u);
         unsigned m[UNR1];
         int tot = 0;
 #pragma unroll
@@ -724,7 +735,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
       hdr[12] = (int)(nc1 - nc0);
     }
     float T;
-    int32_t *R = table + (H >> 1);
+    int32_t *R = table + (Ha >> 1);
     bool collected = false;  // R already gathered (by the previous round's bound)
     if constexpr (KPL == 1) {
       // The previous round's bound of this row is a valid T (all current friends
