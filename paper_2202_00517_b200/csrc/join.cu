@@ -404,7 +404,9 @@ struct SmemLayout {
 };
 
 constexpr int NBIN = 256;        // histogram-select buckets per pass
-constexpr int LSTAGE_ROWS = 16;  // per-warp staged rows in the global-table class
+constexpr int LSTAGE_FLOATS = 1536;  // per-warp staging (6 KB, two buffers) in the global-table class
+// per-warp staging floats of the global-table class: 6 KB, and at least 2 x 8 rows
+__host__ __device__ inline int lstage_floats(int ld) { return LSTAGE_FLOATS > 16 * ld ? LSTAGE_FLOATS : 16 * ld; }
 
 __host__ __device__ inline SmemLayout smem_layout(int G, bool gtab, int d, int ld, int H, int SW) {
   SmemLayout L;
@@ -433,7 +435,7 @@ __host__ __device__ inline SmemLayout smem_layout(int G, bool gtab, int d, int l
     L.list = o;
     o = al16(o + (size_t)(H / 2) * 4);
   } else {
-    size_t st = (size_t)(G / 32) * LSTAGE_ROWS * ld * 4;
+    size_t st = (size_t)(G / 32) * lstage_floats(ld) * 4;
     const size_t st64 = (size_t)32 * ((d + 1) | 1) * 8;  // fp64 rows of d (KL) or d+1 (L2) doubles
     if (st < st64) st = st64;
     L.stage = o;
@@ -501,8 +503,8 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     slabS = slab;
     table = slab + SW;
     list = table + H;
-    wrows = LSTAGE_ROWS / 2;  // two buffers per warp
-    wstage = reinterpret_cast<float *>(sm + L.stage) + (size_t)warp * LSTAGE_ROWS * p.ld;
+    wrows = min(32, lstage_floats(p.ld) / (2 * p.ld));  // rows per buffer, two buffers per warp
+    wstage = reinterpret_cast<float *>(sm + L.stage) + (size_t)warp * lstage_floats(p.ld);
     stage64 = reinterpret_cast<double *>(sm + L.stage);
     rcap64 = 32;
   } else {
