@@ -153,12 +153,21 @@ class PeerTables:
         return 1 if table.data_ptr() == self.bufs[0].data_ptr() else 0
 
 
+_PEER_CACHE: dict = {}
+
+
 def symmetric_peer_tables(eng: "Engine") -> PeerTables:
     """Both tables in torch symmetric memory (CUDA IPC mappings of every rank's
-    buffer over NVLink), rendezvoused once per engine."""
+    buffer over NVLink).  The mapping is a collective (a rendezvous of every
+    rank), so it is made once per (device, table shape, group) and reused by
+    later descents — each run() returns its table to the host before the next
+    one starts."""
     import torch.distributed._symmetric_memory as symm
 
     group = eng.group if eng.group is not None else dist.group.WORLD
+    key = (eng.device, eng.shard.padded_rows, eng.k, group.group_name)
+    if key in _PEER_CACHE:
+        return _PEER_CACHE[key]
     bufs, handles = [], []
     for _ in range(2):
         t = symm.empty((eng.shard.padded_rows, eng.k), dtype=torch.int32, device=eng.device)
@@ -166,7 +175,9 @@ def symmetric_peer_tables(eng: "Engine") -> PeerTables:
         bufs.append(t)
     me, world = eng.shard.rank, eng.shard.world
     peers = [[int(h.buffer_ptrs[r]) for r in range(world) if r != me] for h in handles]
-    return PeerTables(bufs, peers, lambda i: handles[i].barrier(channel=0))
+    pt = PeerTables(bufs, peers, lambda i: handles[i].barrier(channel=0))
+    _PEER_CACHE[key] = pt
+    return pt
 
 
 def exchange_mode(eng: "Engine") -> str:

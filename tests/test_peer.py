@@ -123,6 +123,7 @@ def test_symmetric_peer_tables_world1(cuda):
         pt = symmetric_peer_tables(eng)
         assert [b.shape for b in pt.bufs] == [(1000, 20), (1000, 20)]
         assert pt.peers == [[], []]
+        assert symmetric_peer_tables(Engine(1000, 20, cuda)) is pt  # one mapping per shape and group
         pt.bufs[0].fill_(3)
         pt.barrier(0)
         pt.barrier(1)
