@@ -165,7 +165,7 @@ def symmetric_peer_tables(eng: "Engine") -> PeerTables:
     import torch.distributed._symmetric_memory as symm
 
     group = eng.group if eng.group is not None else dist.group.WORLD
-    key = (eng.device, eng.shard.padded_rows, eng.k, group.group_name)
+    key = (eng.device, eng.shard.padded_rows, eng.k, group.group_name, id(group))
     if key in _PEER_CACHE:
         return _PEER_CACHE[key]
     bufs, handles = [], []
