@@ -284,7 +284,8 @@ def b200_arm(args):
     bytes_per_cmp = 4 * d
     achieved = bytes_per_cmp * join_comps / (join_ms / 1e3) / 1e9 if join_ms > 0 else 0.0
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": ncu_traffic(args.config), "kernel": "knnd_local_join (classify + size-class join launches)",
+            "traffic": ncu_traffic(args.config)[0], "traffic_launch": ncu_traffic(args.config)[1],
+            "kernel": "knnd_local_join (classify + size-class join launches)",
             "bytes_per_comparison": bytes_per_cmp, "peak_source": peak_src,
             "comparisons_per_s": join_comps / (join_ms / 1e3) if join_ms > 0 else 0.0,
             "share_of_step": join_ms / sum(step_ms) if step_ms else None}
@@ -363,12 +364,18 @@ def b200_arm(args):
 
 
 def ncu_traffic(config):
-    """dram bytes per local-join launch from the committed ncu summary, if any."""
+    """(dram bytes of the captured local-join launch, that launch's record) from
+    the committed ncu summary (profiles/ncu_join_<config>.json), if any: DRAM
+    read+write bytes of one W1 launch against its algorithmic bytes (80 B per
+    comparison) — below 1 because the log table mostly lives in L2."""
     path = os.path.join(ROOT, "profiles", f"ncu_join_{config}.json")
     if not os.path.exists(path):
-        return None
+        return None, None
     with open(path) as fh:
-        return json.load(fh).get("dram_bytes_per_launch")
+        rec = json.load(fh)
+    return rec.get("dram_bytes_per_launch"), {k: rec[k] for k in ("capture", "comparisons",
+                                                                  "algorithmic_bytes_per_launch",
+                                                                  "dram_over_algorithmic") if k in rec}
 
 
 def main():

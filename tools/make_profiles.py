@@ -10,6 +10,7 @@
 import csv, json, os, subprocess, sys
 
 tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+SKIP = 9  # the ncu capture's -s (W1 launches skipped)
 G = "gpurun_out"
 P = "profiles"
 os.makedirs(P, exist_ok=True)
@@ -58,7 +59,19 @@ if os.path.exists(rep):
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     dram = rd * scale.get(ru, 1) + wr * scale.get(wu, 1)
     dur, du = metric("gpu__time_duration.sum")
-    json.dump({"capture": f"{tag}: ncu --set full, one W1 join_warp_kernel launch of a C3 bench step",
-               "dram_bytes_per_launch": dram, "duration": [dur, du]}, open(os.path.join(P, "ncu_join_c3.json"), "w"),
-              indent=1)
+    # the captured launch's comparisons: the ncu command ran with KNND_CLASS_TIMING=1,
+    # which prints one line per class launch; the capture is the (skip+1)-th W1 line
+    comps = None
+    logp = os.path.join(G, "ncu_bench_full.log")
+    if os.path.exists(logp):
+        w1 = [int(l.split(" anchors, ")[1].split(" ")[0]) for l in open(logp) if " kind 0 " in l and "anchors," in l]
+        if len(w1) > SKIP:
+            comps = w1[SKIP]
+    out = {"capture": f"{tag}: ncu --set full, one W1 join_warp_kernel launch of a C3 bench step "
+                      f"(launch index {SKIP}: round 3 of the second descent)",
+           "dram_bytes_per_launch": dram, "duration": [dur, du]}
+    if comps:
+        out.update({"comparisons": comps, "algorithmic_bytes_per_launch": 80 * comps,
+                    "dram_over_algorithmic": dram / (80 * comps)})
+    json.dump(out, open(os.path.join(P, "ncu_join_c3.json"), "w"), indent=1)
 print(sorted(os.listdir(P)))
