@@ -479,7 +479,7 @@ __device__ __forceinline__ void hist_find(const int *hist, int target, int *hdr,
   }
 }
 
-template <int G, int NV4, int KPL, bool GTAB>
+template <int G, int NV4, int KPL, bool GTAB, bool PF>
 __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__restrict__ alist,
                                                  const int32_t *__restrict__ acount, int logH, int SW,
                                                  int32_t *__restrict__ gslab, int64_t slab_ints) {
@@ -612,7 +612,66 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
 
     // ---- phase 1: pre-dedup enumeration + hash dedup (one list atomic per warp
     // and group of UNR1 ids per thread)
-    {
+    if constexpr (PF) {
+      // ids two groups ahead (as in join_warp_kernel): a group's friend-row loads
+      // are issued two iterations before its inserts, the select deferred to then
+      int s = s_init, j = j_init;
+      const int iters = (total + G - 1) / G;
+      int fA[UNR1], vA[UNR1], fB[UNR1], vB[UNR1];  // friend id loaded; S value, or -1 (out) / -2 (use friend)
+      auto load_group = [&](int (&f)[UNR1], int (&v)[UNR1], int it0) {
+#pragma unroll
+        for (int u = 0; u < UNR1; ++u) {
+          const int e = (it0 + u) * G + tid;
+          const bool in = e < total;
+          const int sv = S[in ? s : 0];
+          f[u] = __ldg(p.F + (int64_t)sv * K + (j > 0 ? j - 1 : 0));
+          v[u] = in ? (j == 0 ? sv : -2) : -1;
+          s += Gq;
+          j += Gr;
+          const bool wrap = j >= K1;
+          j -= wrap ? K1 : 0;
+          s += wrap ? 1 : 0;
+        }
+      };
+      load_group(fA, vA, 0);
+      load_group(fB, vB, UNR1);
+      for (int it = 0; it < iters; it += UNR1) {
+        int id[UNR1];
+#pragma unroll
+        for (int u = 0; u < UNR1; ++u) {
+          id[u] = vA[u] == -2 ? fA[u] : vA[u];
+          fA[u] = fB[u];
+          vA[u] = vB[u];
+        }
+        if (it + 2 * UNR1 < iters) {
+          load_group(fB, vB, it + 2 * UNR1);
+        } else {
+#pragma unroll
+          for (int u = 0; u < UNR1; ++u) vB[u] = -1;
+        }
+        bool nw[UNR1];
+#pragma unroll
+        for (int u = 0; u < UNR1; ++u)
+          nw[u] = id[u] >= 0 && id[u] != x && hash_insert_cas(table, id[u], sha, (unsigned)Ha - 1u);
+        unsigned m[UNR1];
+        int tot = 0;
+#pragma unroll
+        for (int u = 0; u < UNR1; ++u) {
+          m[u] = __ballot_sync(FULL, nw[u]);
+          tot += __popc(m[u]);
+        }
+        if (tot) {
+          int b0 = 0;
+          if (lane == 0) b0 = atomicAdd(&hdr[0], tot);
+          b0 = __shfl_sync(FULL, b0, 0);
+#pragma unroll
+          for (int u = 0; u < UNR1; ++u) {
+            if (nw[u]) list[b0 + __popc(m[u] & lanemask_lt())] = id[u];
+            b0 += __popc(m[u]);
+          }
+        }
+      }
+    } else {
       int s = s_init, j = j_init;
       const int iters = (total + G - 1) / G;
       for (int it = 0; it < iters; it += UNR1) {
@@ -1390,7 +1449,9 @@ static Plan make_plan(int64_t m, int d, int K, int max_indeg) {
 template <int G, int NV4, int KPL, bool GTAB>
 static int launch_join(const JoinParams &p, const int32_t *alist, const int32_t *acount, int logH, int SW,
                        int32_t *gslab, int64_t slab_ints, int grid_cap, cudaStream_t st) {
-  auto kern = join_kernel<G, NV4, KPL, GTAB>;
+  // friend ids two groups ahead pays for the larger shared tables (B128 at 2^13:
+  // -8%); at 2^12 (at most 4 groups per anchor) it measured 20% slower
+  auto kern = (!GTAB && logH >= 13) ? join_kernel<G, NV4, KPL, GTAB, !GTAB> : join_kernel<G, NV4, KPL, GTAB, false>;
   const SmemLayout L = smem_layout(G, GTAB, p.d, p.ld, 1 << logH, SW);
   const size_t smem = L.total;
   if (smem > 227 * 1024) {
