@@ -1625,42 +1625,9 @@ static int join_run(const char *who, JoinParams &p, int64_t n, int32_t dplan, in
   // diagnostics: KNND_CLASS_TIMING=1 times each class (synchronising) and prints
   // anchors / comparisons / ms per class to stderr
   static const bool timing = getenv("KNND_CLASS_TIMING") != nullptr;
-  // The hub class (global-memory tables) runs on a side stream, concurrently
-  // with the shared-memory classes: its few anchors are latency-bound (one
-  // block per hub), and serialised they left most SMs idle for 0.1-0.3 ms per
-  // round.  Its persistent blocks that find no anchor exit at once, so the
-  // other classes fill the machine around the busy ones.  One side stream and
-  // two events per host thread and device (created on first use).
-  static const bool serial_hubs = getenv("KNND_SERIAL_HUBS") != nullptr;
-  const int ig = P.ncls - 1;  // the global-table class
-  const bool side = !timing && !serial_hubs && P.c[ig].need && P.c[ig].kind == KIND_GLOBAL && ig > 0;
-  cudaEvent_t ev_join = nullptr;
-  if (side) {
-    struct Side {
-      int dev = -1;
-      cudaStream_t s = nullptr;
-      cudaEvent_t fork = nullptr, join = nullptr;
-    };
-    static thread_local Side sides[16];
-    int dev = 0;
-    KNND_CUDA(cudaGetDevice(&dev));
-    Side &sd = sides[dev & 15];
-    if (sd.dev != dev || !sd.s) {
-      KNND_CUDA(cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking));
-      KNND_CUDA(cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming));
-      KNND_CUDA(cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming));
-      sd.dev = dev;
-    }
-    ev_join = sd.join;
-    KNND_CUDA(cudaEventRecord(sd.fork, st));
-    KNND_CUDA(cudaStreamWaitEvent(sd.s, sd.fork, 0));
-    const int rc = dispatch_class(P, ig, p, lists, counts, m, slabs, glists, sd.s);
-    if (rc) return rc;
-    KNND_CUDA(cudaEventRecord(sd.join, sd.s));
-  }
   // biggest tables first: the few long hub anchors start early
   for (int i = P.ncls - 1; i >= 0; --i) {
-    if (!P.c[i].need || (side && i == ig)) continue;
+    if (!P.c[i].need) continue;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     unsigned long long t0[4] = {0, 0, 0, 0};
     if (timing) {
@@ -1688,7 +1655,6 @@ static int join_run(const char *who, JoinParams &p, int64_t n, int32_t dplan, in
       cudaEventDestroy(e1);
     }
   }
-  if (side) KNND_CUDA(cudaStreamWaitEvent(st, ev_join, 0));  // the hub rows are part of this call's output
   return KNND_OK;
 }
 
