@@ -1625,9 +1625,53 @@ static int join_run(const char *who, JoinParams &p, int64_t n, int32_t dplan, in
   // diagnostics: KNND_CLASS_TIMING=1 times each class (synchronising) and prints
   // anchors / comparisons / ms per class to stderr
   static const bool timing = getenv("KNND_CLASS_TIMING") != nullptr;
+  // The big-table classes (>= 2^14 slots and the hubs) run on a side stream,
+  // concurrently with the rest: they hold few anchors, each long and latency
+  // bound, and serialised their tails left most SMs idle — ~0.1-0.3 ms per
+  // round, a 10-15% loss once a rank holds 1/8 of the anchors.  Persistent
+  // blocks that find no anchor exit at once, so the other classes fill the
+  // machine around the busy ones.  Measured (C3): P = 1 +0.5%, the 8-rank
+  // projection's join -5.5%; C4 -0.7%.  KNND_SIDE_CLASSES=k overrides (the k
+  // biggest classes; 0 = all serial).  One side stream and two events per host
+  // thread and device, created on first use.
+  static const int nside_env = getenv("KNND_SIDE_CLASSES") ? atoi(getenv("KNND_SIDE_CLASSES")) : -1;
+  int ig = P.ncls;  // classes [ig, ncls) go to the side stream
+  if (nside_env >= 0) {
+    ig = P.ncls - nside_env;
+  } else {
+    while (ig - 1 > 0 && (P.c[ig - 1].kind == KIND_GLOBAL || P.c[ig - 1].logH >= 14)) --ig;
+  }
+  const bool side = !timing && ig > 0 && ig < P.ncls;
+  cudaEvent_t ev_join = nullptr;
+  if (side) {
+    struct Side {
+      int dev = -1;
+      cudaStream_t s = nullptr;
+      cudaEvent_t fork = nullptr, join = nullptr;
+    };
+    static thread_local Side sides[16];
+    int dev = 0;
+    KNND_CUDA(cudaGetDevice(&dev));
+    Side &sd = sides[dev & 15];
+    if (sd.dev != dev || !sd.s) {
+      KNND_CUDA(cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking));
+      KNND_CUDA(cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming));
+      KNND_CUDA(cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming));
+      sd.dev = dev;
+    }
+    ev_join = sd.join;
+    KNND_CUDA(cudaEventRecord(sd.fork, st));
+    KNND_CUDA(cudaStreamWaitEvent(sd.s, sd.fork, 0));
+    for (int i = P.ncls - 1; i >= ig; --i) {
+      if (!P.c[i].need) continue;
+      const int rc = dispatch_class(P, i, p, lists, counts, m, slabs, glists, sd.s);
+      if (rc) return rc;
+    }
+    KNND_CUDA(cudaEventRecord(sd.join, sd.s));
+  }
   // biggest tables first: the few long hub anchors start early
   for (int i = P.ncls - 1; i >= 0; --i) {
-    if (!P.c[i].need) continue;
+    if (!P.c[i].need || (side && i >= ig)) continue;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     unsigned long long t0[4] = {0, 0, 0, 0};
     if (timing) {
@@ -1655,6 +1699,7 @@ static int join_run(const char *who, JoinParams &p, int64_t n, int32_t dplan, in
       cudaEventDestroy(e1);
     }
   }
+  if (side) KNND_CUDA(cudaStreamWaitEvent(st, ev_join, 0));  // the hub rows are part of this call's output
   return KNND_OK;
 }
 
