@@ -90,11 +90,17 @@ template <int KPL>
 __global__ void sort_rows_kernel(const double *__restrict__ pts, int pstride, const double *__restrict__ log64,
                                  int d64, const double *__restrict__ xlogx, int d, int metric, int K, int64_t lo,
                                  int64_t hi, const int32_t *__restrict__ draws, int32_t *__restrict__ out_ids,
-                                 double *__restrict__ out_kl) {
-  extern __shared__ double sx[];  // per warp: d doubles
+                                 double *__restrict__ out_kl, int staged) {
+  // per warp: d doubles (the anchor), then (staged) K rows of d64 doubles at an
+  // odd stride: the K candidate rows are copied in row-contiguous 8 B chunks
+  // (cp.async) instead of one lane reading one scattered row
+  extern __shared__ double sx[];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
-  double *x64 = sx + (size_t)w * d;
+  const int sd = d64 | 1;
+  const size_t per_warp = (size_t)d + (staged ? (size_t)K * sd : 0);
+  double *x64 = sx + (size_t)w * per_warp;
+  double *stage = x64 + d;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t x = lo + (int64_t)blockIdx.x * (blockDim.x >> 5) + w; x < hi; x += warps) {
     const int64_t xr = x - lo;
@@ -103,15 +109,42 @@ __global__ void sort_rows_kernel(const double *__restrict__ pts, int pstride, co
     const double xl = xlogx[x];
     KeyD key[KPL];
     int idv[KPL];
+    if (KPL == 1 && staged) {
+      const int y = lane < K ? draws[xr * K + lane] : 0;
+      idv[0] = lane < K ? y : -1;
+      const int nchunk = K * d64;
+      int r = lane / d64, j = lane - (lane / d64) * d64;
+      const int rq = 32 / d64, rr = 32 - rq * d64;
+      for (int c0 = 0; c0 < nchunk; c0 += 32) {
+        const int yr = __shfl_sync(FULL, y, r & 31);
+        if (c0 + lane < nchunk) cp_async8(stage + r * sd + j, log64 + (int64_t)yr * d64 + j);
+        r += rq;
+        j += rr;
+        if (j >= d64) {
+          j -= d64;
+          ++r;
+        }
+      }
+      cp_async_wait_all();
+      __syncwarp();
+      key[0] = KeyD::inf();
+      if (lane < K) {  // exact_score_m's arithmetic, from the staged row
+        const double *row = stage + lane * sd;
+        double acc = 0.0;
+        for (int jj = 0; jj < d; ++jj) acc = fma(x64[jj], row[jj], acc);
+        key[0] = {finish_score(metric, xl, metric == METRIC_L2 ? row[d] : 0.0, acc), lane};
+      }
+    } else {
 #pragma unroll
-    for (int q = 0; q < KPL; ++q) {
-      int pos = q * 32 + lane;
-      key[q] = KeyD::inf();
-      idv[q] = -1;
-      if (pos < K) {
-        int y = draws[xr * K + pos];
-        idv[q] = y;
-        key[q] = {exact_score_m(x64, log64 + (int64_t)y * d64, d, xl, metric), pos};
+      for (int q = 0; q < KPL; ++q) {
+        int pos = q * 32 + lane;
+        key[q] = KeyD::inf();
+        idv[q] = -1;
+        if (pos < K) {
+          int y = draws[xr * K + pos];
+          idv[q] = y;
+          key[q] = {exact_score_m(x64, log64 + (int64_t)y * d64, d, xl, metric), pos};
+        }
       }
     }
     // sort keys; the tie field is the draw position (stable argsort)
@@ -240,13 +273,17 @@ static int sort_rows_impl(const char *who, const double *pts, int pstride, const
   int64_t rows = row_hi - row_lo;
   int64_t blocks = (rows + wpb - 1) / wpb;
   if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
-  size_t smem = (size_t)wpb * d * sizeof(double);
-  if (k <= 32)
+  const size_t staged_smem = (size_t)wpb * (d + (size_t)k * (d64 | 1)) * sizeof(double);
+  const int staged = (k <= 32 && staged_smem <= 160 * 1024) ? 1 : 0;
+  size_t smem = staged ? staged_smem : (size_t)wpb * d * sizeof(double);
+  if (k <= 32) {
+    KNND_CUDA(cudaFuncSetAttribute(sort_rows_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     sort_rows_kernel<1><<<(unsigned)blocks, threads, smem, as_stream(stream)>>>(
-        pts, pstride, log64, d64, xlogx, d, metric, k, row_lo, row_hi, draws, out_ids, out_kl);
-  else
+        pts, pstride, log64, d64, xlogx, d, metric, k, row_lo, row_hi, draws, out_ids, out_kl, staged);
+  } else {
     sort_rows_kernel<2><<<(unsigned)blocks, threads, smem, as_stream(stream)>>>(
-        pts, pstride, log64, d64, xlogx, d, metric, k, row_lo, row_hi, draws, out_ids, out_kl);
+        pts, pstride, log64, d64, xlogx, d, metric, k, row_lo, row_hi, draws, out_ids, out_kl, staged);
+  }
   KNND_LAUNCHED(1);
   return KNND_OK;
 }
