@@ -222,10 +222,26 @@ def b200_arm(args):
     pts = b2.sample_simplex_uniform(d, n, b2.derive_rng(seed, b2.STREAM_DATA, d))
     rs = b2.KlRankingSystem(pts, validate=False)
     tabs = rs.device_tables(dev)
+    t0 = time.perf_counter()
     draws = b2.random_kout_draws(n, k, b2.derive_rng(seed, b2.STREAM_INIT))
+    init_host_ms = (time.perf_counter() - t0) * 1e3
     eng = Engine(n, k, dev)
     draws_dev = eng.alloc_table()
     eng.upload_rows(draws, draws_dev)
+    # the same draws on the device (knnd_random_kout, what run() uses), timed and checked
+    from paper_2202_00517_b200.descent import device_random_kout
+
+    init_dev_ms = None
+    if n - 1 > 2 * k * k:
+        tmp = eng.alloc_table()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        device_random_kout(eng, n, k, b2.derive_rng(seed, b2.STREAM_INIT), tmp)
+        torch.cuda.synchronize()
+        init_dev_ms = (time.perf_counter() - t0) * 1e3
+        s_ = eng.shard
+        assert torch.equal(tmp[s_.lo:s_.hi], draws_dev[s_.lo:s_.hi]), "device init draws differ from numpy's"
+        del tmp
     smp_dev = _to_device(draw_fcc_schedule(n, k, cfg, max_rounds), dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
     stream = torch.cuda.current_stream(dev)
@@ -348,8 +364,12 @@ def b200_arm(args):
             "config": {"workload": workload_desc(args.config, n, d, k), "n": n, "d": d, "k": k, "seed": seed,
                        "rounds_per_step": rounds, "comparisons_per_step": comps // max(args.steps, 1),
                        "time_to_termination_ms": statistics.mean(step_ms),
+                       "init_draws_ms": {"host_numpy": init_host_ms, "device_knnd_random_kout": init_dev_ms,
+                                         "note": "input generation, outside `value`; run() (e2e) uses the device draws"},
                        "l2": "flushed (256 MiB write) before every step",
-                       "parallelism": f"row-shard x{world}" + (" + NCCL all-gather" if world > 1 else "")},
+                       "parallelism": f"row-shard x{world}" + ((" + rows stored into every rank's table during the join"
+                                                                " (symmetric memory over NVLink)" if eng.peer is not None
+                                                                else " + NCCL all-gather") if world > 1 else "")},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "time_to_termination_s": tt.item() / max(args.e2e_steps, 1)},
             "gpu_launches": launches_total,
