@@ -234,11 +234,12 @@ def b200_arm(args):
     init_dev_ms = None
     if n - 1 > 2 * k * k:
         tmp = eng.alloc_table()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        device_random_kout(eng, n, k, b2.derive_rng(seed, b2.STREAM_INIT), tmp)
-        torch.cuda.synchronize()
-        init_dev_ms = (time.perf_counter() - t0) * 1e3
+        for _ in range(2):  # the second call is timed (the first loads the module)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            device_random_kout(eng, n, k, b2.derive_rng(seed, b2.STREAM_INIT), tmp)
+            torch.cuda.synchronize()
+            init_dev_ms = (time.perf_counter() - t0) * 1e3
         s_ = eng.shard
         assert torch.equal(tmp[s_.lo:s_.hi], draws_dev[s_.lo:s_.hi]), "device init draws differ from numpy's"
         del tmp
