@@ -307,6 +307,10 @@ def b200_arm(args):
             "comparisons_per_s": join_comps / (join_ms / 1e3) if join_ms > 0 else 0.0,
             "share_of_step": join_ms / sum(step_ms) if step_ms else None}
 
+    # the final table of the last timed step, on the host before anything else
+    # runs (under the fused exchange the device tables are reused by later descents)
+    if rank == 0 and not args.no_recall:
+        last["state"].friends
     # ---- end to end through the public API from host buffers
     e2e_s, e2e_comps = 0.0, 0
     h2d = d2h = 0
