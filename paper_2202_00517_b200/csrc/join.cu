@@ -168,6 +168,30 @@ __device__ __forceinline__ void stage_rows_f32_reg(float *stage, const float *__
   }
 }
 
+// the warp kernel's variant of stage_rows_f32_reg: every lane executes every
+// shuffle, the copies are predicated, fixed unrolled iterations (the block
+// kernels measured slower with it)
+template <int NV4>
+__device__ __forceinline__ void stage_rows_f32_reg_full(float *stage, const float *__restrict__ log32, int idreg,
+                                                        int nrow, int lane) {
+  constexpr int ld = NV4 * 4;
+  constexpr int rpi = 32 / NV4;
+  constexpr int ITERS = (32 + rpi - 1) / rpi;  // nrow <= 32: a fixed, fully unrolled count
+  const int r0 = lane / NV4, part = lane - r0 * NV4;
+  const unsigned dst = smem_u32(stage) + (unsigned)(r0 * ld + part * 4) * 4u;
+  const float *src = log32 + part * 4;
+  const bool lane_on = r0 < rpi;
+#pragma unroll
+  for (int t = 0; t < ITERS; ++t) {
+    const int r = r0 + t * rpi;
+    const int y = __shfl_sync(FULL, idreg, r & 31);
+    if (t * rpi < nrow && lane_on && r < nrow)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + (unsigned)(t * rpi * ld * 4)),
+                   "l"(src + (int64_t)y * ld)
+                   : "memory");
+  }
+}
+
 // ce = -sum x*l and ab = sum |x*l| of one staged row (left to right).  With
 // nonpos (all logs <= 0) every term of ab equals the term of ce, so ab == ce
 // bit for bit and only one accumulator is needed.
@@ -1140,7 +1164,7 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
     int id_after = (rows + lane < U && lane < rows) ? list[rows + lane] : 0;
     if (U > 0) {
       if constexpr (NV4 > 0)
-        stage_rows_f32_reg<NV4>(stage, p.log32, id_next, min(rows, U), lane);
+        stage_rows_f32_reg_full<NV4>(stage, p.log32, id_next, min(rows, U), lane);
       else
         stage_rows_f32<NV4>(stage, p.log32, list, min(rows, U), ld, lane);
       cp_async_commit();
@@ -1150,7 +1174,7 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
       if (k0 + rows < U) {  // prefetch the next batch into the other buffer
         const int n1 = min(rows, U - k0 - rows);
         if constexpr (NV4 > 0)
-          stage_rows_f32_reg<NV4>(stage + (buf ^ 1) * rows * ld, p.log32, id_after, n1, lane);
+          stage_rows_f32_reg_full<NV4>(stage + (buf ^ 1) * rows * ld, p.log32, id_after, n1, lane);
         else
           stage_rows_f32<NV4>(stage + (buf ^ 1) * rows * ld, p.log32, list + k0 + rows, n1, ld, lane);
         cp_async_commit();
