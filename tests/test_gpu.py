@@ -369,3 +369,49 @@ def test_c4_trajectory(cuda, trajectories):
     rec = load_json("recall.json")
     if "c4" in rec:
         _recall_check("c4", pts, final, rec, 10_000)
+
+
+_SIDE_SCRIPT = r"""
+import sys, hashlib
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import numpy as np, torch
+import paper_2202_00517_b200 as b2
+from oracle import port, native
+from test_gpu import _hub_table
+n, d, k = 30000, 20, 20
+rng = np.random.default_rng(n + d + k)
+pts = port.experiment_points(n, d, 3)
+hubs = [(7, n // 4), (11, n // 10), (13, 40 * k), (17, 8 * k), (19, 3 * k), (23, 2 * k)]
+table = native.sort_rows(native.Tables(pts), _hub_table(n, k, hubs, rng))
+rs = b2.KlRankingSystem(pts, validate=False)
+st = b2.KnnState(table)
+out = torch.empty((n, k), dtype=torch.int32, device="cuda")
+uc = torch.empty(n, dtype=torch.int32, device="cuda")
+tally = torch.zeros(4, dtype=torch.int64, device="cuda")
+st._engine.ops.join(rs.device_tables(), st._table, n, k, st._csr, st._max_indeg, out, tally, None, uc)
+h = hashlib.sha256(out.cpu().numpy().tobytes() + uc.cpu().numpy().tobytes()).hexdigest()
+print("RESULT", h, tally.cpu().tolist()[:3])
+"""
+
+
+def test_class_streams_do_not_change_results(cuda):
+    """The big-table classes run on a side stream by default; all classes on the
+    launching stream (KNND_SIDE_CLASSES=0), or more of them on the side stream,
+    give the same rows, |U| and tallies (the setting is read once per process,
+    hence the subprocesses)."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    code = _SIDE_SCRIPT.format(root=os.path.dirname(here), tests=here)
+    outs = []
+    for side in (None, "0", "4"):
+        env = dict(os.environ)
+        env.pop("KNND_SIDE_CLASSES", None)
+        if side is not None:
+            env["KNND_SIDE_CLASSES"] = side
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append([line for line in r.stdout.splitlines() if line.startswith("RESULT")][-1])
+    assert outs[0] == outs[1] == outs[2], outs
