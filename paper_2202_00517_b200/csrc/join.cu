@@ -110,6 +110,39 @@ __device__ __forceinline__ bool hash_insert_cas(int32_t *table, int y, unsigned 
   }
 }
 
+// UNR1 inserts of one lane with their first probes issued together: the
+// bucket reads, then the CAS of every id that saw its bucket without it and
+// with a free slot, all predicated (no per-id branches); an id whose CAS lost
+// (another id took the slot) or whose bucket was full takes the probing loop.
+// Same outcome as UNR1 calls of hash_insert_cas: an id is new exactly once.
+__device__ __forceinline__ void hash_insert4(int32_t *table, const int (&id)[UNR1], int x, unsigned shift,
+                                             unsigned mask, bool (&nw)[UNR1]) {
+  unsigned b[UNR1];
+  int4 v[UNR1];
+  bool valid[UNR1];
+#pragma unroll
+  for (int u = 0; u < UNR1; ++u) {
+    valid[u] = id[u] >= 0 && id[u] != x;
+    b[u] = hash_slot(id[u], shift + 2);
+    v[u] = valid[u] ? reinterpret_cast<const int4 *>(table)[b[u]] : make_int4(0, 0, 0, 0);
+  }
+  int prev[UNR1];
+  bool retry[UNR1];
+#pragma unroll
+  for (int u = 0; u < UNR1; ++u) {
+    const int y = id[u];
+    const bool found = (v[u].x == y) | (v[u].y == y) | (v[u].z == y) | (v[u].w == y);
+    const bool can = valid[u] && !found && v[u].w == EMPTY;
+    const int occ = 4 + (v[u].x >> 31) + (v[u].y >> 31) + (v[u].z >> 31) + (v[u].w >> 31);
+    prev[u] = can ? atomicCAS(table + b[u] * 4 + occ, EMPTY, y) : EMPTY;  // EMPTY: no CAS made
+    nw[u] = can && prev[u] == EMPTY;
+    retry[u] = valid[u] && !found && !nw[u] && prev[u] != y;
+  }
+#pragma unroll
+  for (int u = 0; u < UNR1; ++u)
+    if (retry[u]) nw[u] = hash_insert_cas(table, id[u], shift, mask);
+}
+
 // warp-aggregated append of `val` (where `take`) to list[*counter ...]
 __device__ __forceinline__ void warp_append(bool take, int val, int *counter, int32_t *list, int lane) {
   const unsigned m = __ballot_sync(FULL, take);
@@ -1130,9 +1163,7 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
         // shared-memory CAS insert (hash_insert_cas): in-warp duplicates resolve in
         // the CAS itself; the ballots append the winners in lane order
         bool nw[UNR1];
-#pragma unroll
-        for (int u = 0; u < UNR1; ++u)
-          nw[u] = id[u] >= 0 && id[u] != x && hash_insert_cas(table, id[u], shift, (unsigned)H - 1u);
+        hash_insert4(table, id, x, shift, (unsigned)H - 1u, nw);
 #pragma unroll
         for (int u = 0; u < UNR1; ++u) {
           const unsigned m = __ballot_sync(FULL, nw[u]);
