@@ -167,10 +167,15 @@ using namespace knnd;
 
 extern "C" {
 
-size_t knnd_random_kout_workspace_bytes(int64_t n, int32_t k) {
+// generator threads the workspace has room for: a rejection rate up to 1/2
+// (the worst case for a range below 2^31) plus margins
+static long long rng_ws_threads(int64_t n, int32_t k) {
   const long long N = n * (long long)k;
-  // room for a rejection rate up to 1/2 (the worst case for a range below 2^31) plus margins
-  const long long nthreads = (N * 21 / 10 + 8192) / (2 * RNG_OUT_PER_THREAD) + 64;
+  return (N * 21 / 10 + 8192) / (2 * RNG_OUT_PER_THREAD) + 64;
+}
+
+size_t knnd_random_kout_workspace_bytes(int64_t n, int32_t k) {
+  const long long nthreads = rng_ws_threads(n, k);
   return align_up(sizeof(Jump), 256) + align_up((size_t)nthreads * 4, 256) + align_up((size_t)nthreads * 8, 256) +
          256;
 }
@@ -209,7 +214,10 @@ int knnd_random_kout(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint
   char *w = static_cast<char *>(ws);
   Jump *dJ = reinterpret_cast<Jump *>(w);
   w += align_up(sizeof(Jump), 256);
-  const long long cap_threads = (long long)((need - align_up(sizeof(Jump), 256) - 256) / 12);
+  // the layout of knnd_random_kout_workspace_bytes exactly (deriving the count
+  // back from the byte total overshot it by the alignment padding, and the
+  // scan's two scalars then landed up to ~0.5 KB past the workspace)
+  const long long cap_threads = rng_ws_threads(n, k);
   int *counts = reinterpret_cast<int *>(w);
   w += align_up((size_t)cap_threads * 4, 256);
   long long *offsets = reinterpret_cast<long long *>(w);
