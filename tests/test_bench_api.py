@@ -2,10 +2,12 @@
 reference's own reports (tests/golden/bench_reports.json, recorded by
 make_bench_golden.py from rankdescent.bench, bench.py:136-267)."""
 
+import numpy as np
 import pytest
 
 from conftest import load_json
 
+import paper_2202_00517_b200 as b2
 from paper_2202_00517_b200 import ConfigError, RoundStats
 from paper_2202_00517_b200 import bench as xb
 
@@ -92,3 +94,35 @@ def test_dimension_sweep_matches_reference(golden, cuda):
         got = [[r.round_index, r.fcc, r.comparisons, r.changed_friend_sets] for r in rep.rounds]
         assert got == rec["rounds"]
         assert (rep.rounds_used, rep.final_fcc, rep.recall) == (rec["rounds_used"], rec["final_fcc"], rec["recall"])
+
+
+def _small(**kw):
+    base = dict(n=300, d=5, k=6, seed=3)
+    base.update(kw)
+    return xb.ExperimentSpec(**base)
+
+
+@pytest.mark.gpu
+def test_report_shape_and_reproducibility(cuda):
+    """bench.py behaviours the reference's test_bench.py pins: report fields,
+    reproducible modulo wall clock, worker count and singleton sweeps change
+    nothing, recall modes, parseable CSV rows."""
+    import csv
+    import io
+    import json
+
+    a = xb.run_experiment(_small())
+    assert a.rounds_used == len(a.rounds) >= 1 and a.round_budget == b2.round_budget(300, 6)
+    assert a.final_fcc == a.rounds[-1].fcc and 0.0 <= a.recall <= 1.0 and a.friend_map.shape == (300, 6)
+    b = xb.run_experiment(_small(workers=4))
+    assert np.array_equal(a.friend_map, b.friend_map) and a.recall == b.recall
+    assert [r.comparisons for r in a.rounds] == [r.comparisons for r in b.rounds]
+    (swept,) = xb.dimension_sweep(_small(), [5])
+    assert np.array_equal(swept.friend_map, a.friend_map) and swept.recall == a.recall
+    assert xb.run_experiment(_small(recall_mode="off")).recall is None
+    assert xb.run_experiment(_small(ranking="euclidean")).recall > 0.5
+    obj = json.loads(xb.emit_report(a, "json"))
+    assert obj["summary"]["final_fcc"] == a.final_fcc and obj["summary"]["recall"] == a.recall
+    rows = list(csv.DictReader(io.StringIO(xb.emit_report(a, "csv"))))
+    assert len(rows) == a.rounds_used + 1 and rows[-1]["record"] == "summary"
+    assert [int(r["round_index"]) for r in rows[:-1]] == list(range(1, a.rounds_used + 1))
