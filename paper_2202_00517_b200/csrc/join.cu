@@ -707,9 +707,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
           for (int u = 0; u < UNR1; ++u) vB[u] = -1;
         }
         bool nw[UNR1];
-#pragma unroll
-        for (int u = 0; u < UNR1; ++u)
-          nw[u] = id[u] >= 0 && id[u] != x && hash_insert_cas(table, id[u], sha, (unsigned)Ha - 1u);
+        hash_insert4(table, id, x, sha, (unsigned)Ha - 1u, nw);
         unsigned m[UNR1];
         int tot = 0;
 #pragma unroll
