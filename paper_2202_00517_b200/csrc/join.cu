@@ -1038,7 +1038,7 @@ __device__ __forceinline__ void prefetch_anchor(const JoinParams &p, int x, int6
   cp_async_commit();
 }
 
-template <int NV4, int KPL, bool GLIST>
+template <int NV4, int KPL, bool GLIST, bool VF>
 __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
     join_warp_kernel(JoinParams p, const int32_t *__restrict__ alist, const int32_t *__restrict__ acount, int logH,
                      int SW, int32_t *__restrict__ glists) {
@@ -1119,7 +1119,53 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
 
     // ---- phase 1: dedup
     int U = 0;
-    {
+    if constexpr (VF) {
+      // K % 4 == 0: friend rows read as int4.  Unit u < nF holds ids 4q..4q+3
+      // of F(S[s]) (s = u / K4, q = u % K4); the ceil(nS/4) units after them
+      // hold S itself.  One unit (4 ids) per lane per pass, loaded two passes ahead.
+      const int K4 = K >> 2;
+      const int nF = nS * K4, nU = nF + ((nS + 3) >> 2);
+      const int ds = 32 / K4, dq = 32 - ds * K4;
+      int s = lane / K4, q = lane - (lane / K4) * K4;
+      auto load_unit = [&](int4 &v, int u) {
+        if (u < nF) {
+          v = __ldg(reinterpret_cast<const int4 *>(p.F + (int64_t)S[s] * K) + q);
+        } else if (u < nU) {
+          const int b = (u - nF) * 4;
+          v = reinterpret_cast<const int4 *>(S)[u - nF];
+          v.y = b + 1 < nS ? v.y : -1;
+          v.z = b + 2 < nS ? v.z : -1;
+          v.w = b + 3 < nS ? v.w : -1;
+        } else {
+          v = make_int4(-1, -1, -1, -1);
+        }
+        s += ds;
+        q += dq;
+        const bool wrap = q >= K4;
+        q -= wrap ? K4 : 0;
+        s += wrap ? 1 : 0;
+      };
+      int4 vA, vB;
+      load_unit(vA, lane);
+      load_unit(vB, 32 + lane);
+#pragma unroll 1
+      for (int u0 = 0; u0 < nU; u0 += 32) {
+        const int id[UNR1] = {vA.x, vA.y, vA.z, vA.w};
+        vA = vB;
+        if (u0 + 64 < nU)
+          load_unit(vB, u0 + 64 + lane);
+        else
+          vB = make_int4(-1, -1, -1, -1);
+        bool nw[UNR1];
+        hash_insert4(table, id, x, shift, (unsigned)H - 1u, nw);
+#pragma unroll
+        for (int u = 0; u < UNR1; ++u) {
+          const unsigned m = __ballot_sync(FULL, nw[u]);
+          if (nw[u]) list[U + __popc(m & lanemask_lt())] = id[u];
+          U += __popc(m);
+        }
+      }
+    } else {
       int s = s_init, j = j_init;
       // Pre-dedup ids two groups ahead: the friend-row loads stay in flight until
       // their group is consumed (the select is deferred to that point).  Slot A
@@ -1528,7 +1574,8 @@ static int launch_join(const JoinParams &p, const int32_t *alist, const int32_t 
 template <int NV4, int KPL, bool GLIST>
 static int launch_warp(const JoinParams &p, const int32_t *alist, const int32_t *acount, int logH, int SW,
                        int32_t *glists, cudaStream_t st) {
-  auto kern = join_warp_kernel<NV4, KPL, GLIST>;
+  // friend rows as int4 when they are 16-B aligned (K % 4 == 0)
+  auto kern = (p.K % 4 == 0) ? join_warp_kernel<NV4, KPL, GLIST, true> : join_warp_kernel<NV4, KPL, GLIST, false>;
   WarpSlab L = warp_slab(p.d, p.ld, 1 << logH, SW);
   if (GLIST) L.total = L.list;  // the unique list lives in the global slab
   // warps per block: the largest of 4/2/1 that keeps the most warps resident
