@@ -1098,6 +1098,8 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
     double *x64 = reinterpret_cast<double *>(inb + L.x64);
     int32_t *S = reinterpret_cast<int32_t *>(inb + L.S);
     const int64_t xr = (int64_t)x - p.lo;
+    // the previous round's row bound, loaded now: it is needed after the screen
+    const float T0 = p.bound_in ? __ldg(p.bound_in + xr) : __int_as_float(0x7fc00000);
     const int nS = K + c;
     const int total = nS * K1;
 
@@ -1316,7 +1318,6 @@ __global__ void __launch_bounds__(128, GLIST ? 6 : 4)
       }
       return t;
     };
-    const float T0 = p.bound_in ? p.bound_in[xr] : __int_as_float(0x7fc00000);
     float T;
     if (KPL == 1 && isfinite(T0)) {
       const float th0 = T0 + 2.f * (p.band * am + slack) + fabsf(T0) * 1e-6f;
