@@ -219,3 +219,18 @@ def test_run_to_fixed_point_matches_reference(cuda, cases, name):
     else:
         assert h[-1].changed_friend_sets == 0
     assert_valid_kout(friends, c["n"], c["cfg"]["k"])
+
+
+@pytest.mark.parametrize("n,d,k", [(20_000, 10, 16), (100_000, 20, 20)])
+def test_repeated_runs_on_one_ranking_system_agree(cuda, n, d, k):
+    """run() twice on the same ranking system (cached device tables, reused
+    caching-allocator blocks): identical tables and histories — the check that
+    exposed knnd_random_kout's workspace overrun."""
+    pts = b2.sample_simplex_uniform(d, n, b2.derive_rng(0, b2.STREAM_DATA, d))
+    ds, rs = b2.Dataset(pts), b2.KlRankingSystem(pts, validate=False)
+    cfg = b2.DescentConfig(k=k, seed=1, max_rounds=3)
+    fa, ha = b2.run(ds, rs, cfg)
+    fb, hb = b2.run(ds, rs, cfg)
+    fc, hc = b2.run(ds, b2.KlRankingSystem(pts, validate=False), cfg)
+    assert np.array_equal(fa, fb) and np.array_equal(fa, fc)
+    assert hist(ha) == hist(hb) == hist(hc)
