@@ -21,6 +21,8 @@ WANT = [
     ("L2 sectors (tex) pct of peak", "lts__t_sectors_srcunit_tex.sum.pct_of_peak_sustained_elapsed"),
     ("L2 throughput pct", "lts__throughput.avg.pct_of_peak_sustained_elapsed"),
     ("L2 hit rate", "lts__t_sector_hit_rate.pct"),
+    ("L2 read sectors from the SMs", "lts__t_sectors_srcunit_tex_op_read.sum"),
+    ("L2 -> L1/smem bytes", "l1tex__m_xbar2l1tex_read_bytes.sum"),
     ("L1/shared wavefronts pct", "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
     ("shared-memory wavefronts pct", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
     ("FP32 (FMA pipe) active pct", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
