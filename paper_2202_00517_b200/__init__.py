@@ -10,14 +10,17 @@ initial row sort and FCC statistic in hand-written sm_100a kernels
 The exact K-NN ground truth and recall (evaluation.py:36-137) run on the GPU
 too (knnd_exact_knn).  The KL and squared-Euclidean ranking systems
 (similarity.py:80-140) are accelerated through the same fused join; other
-ranking systems, the metrizability checker and the CLI are out of scope (see
-DESIGN.md).  ``paper_2202_00517_b200.bench`` mirrors the reference's experiment
-harness (run_experiment / dimension_sweep / emit_report / emit_sweep).
+ranking systems, the metrizability checker, the comparator-only engine
+(BoundedNeighborSet), point-file IO and the CLI are out of scope (see
+DESIGN.md).  The experiment harness (run_experiment / dimension_sweep /
+emit_report / emit_sweep, ``paper_2202_00517_b200.bench``) and the small host
+helpers (kl_divergence, candidate_set, build_cofriends, verify_total_order)
+keep the reference's names and behaviour.
 """
 
 from ._lib import EXPORTS, KnndError, launch_count
 from ._lib import load as load_library
-from .core import ConfigError, Dataset, ItemId, RankingSystem, ScoredRankingSystem
+from .core import ConfigError, Dataset, ItemId, RankingSystem, ScoredRankingSystem, build_cofriends, verify_total_order
 from .descent import (
     STREAM_DATA,
     STREAM_FCC,
@@ -33,16 +36,28 @@ from .descent import (
     propose_new_friend_set,
     random_kout_draws,
     round_budget,
+    candidate_set,
     run,
     run_round,
     run_to_fixed_point,
 )
 from . import bench, evaluation
+from .bench import (
+    ORACLE_GUARD,
+    ExperimentReport,
+    ExperimentSpec,
+    OracleGuardError,
+    dimension_sweep,
+    emit_report,
+    emit_sweep,
+    run_experiment,
+)
 from .evaluation import ExactKnnGraph, exact_knn, exact_rows, recall, sampled_recall, uniform_recall_sample
 from .similarity import (
     EuclideanRankingSystem,
     KlRankingSystem,
     euclidean_ranking,
+    kl_divergence,
     sample_simplex_uniform,
     validate_simplex_points,
 )
@@ -50,43 +65,55 @@ from .similarity import (
 __version__ = "0.1.0"
 
 __all__ = [
+    "bench",
+    "build_cofriends",
+    "candidate_set",
     "ConfigError",
     "Dataset",
-    "DescentConfig",
-    "EXPORTS",
-    "EuclideanRankingSystem",
-    "ExactKnnGraph",
-    "ItemId",
-    "KlRankingSystem",
-    "KnndError",
-    "KnnState",
-    "RankingSystem",
-    "RoundStats",
-    "STREAM_DATA",
-    "STREAM_FCC",
-    "STREAM_INIT",
-    "STREAM_RECALL",
-    "ScoredRankingSystem",
     "derive_rng",
+    "DescentConfig",
+    "dimension_sweep",
+    "emit_report",
+    "emit_sweep",
     "euclidean_ranking",
-    "bench",
+    "EuclideanRankingSystem",
     "evaluation",
     "exact_knn",
     "exact_rows",
+    "ExactKnnGraph",
+    "ExperimentReport",
+    "ExperimentSpec",
+    "EXPORTS",
     "fcc_samples",
     "friend_clustering_rate",
     "init_random_kout",
+    "ItemId",
+    "kl_divergence",
+    "KlRankingSystem",
+    "KnndError",
+    "KnnState",
     "launch_count",
     "load_library",
+    "ORACLE_GUARD",
+    "OracleGuardError",
     "propose_new_friend_set",
     "random_kout_draws",
+    "RankingSystem",
     "recall",
     "round_budget",
+    "RoundStats",
     "run",
+    "run_experiment",
     "run_round",
     "run_to_fixed_point",
     "sample_simplex_uniform",
     "sampled_recall",
+    "ScoredRankingSystem",
+    "STREAM_DATA",
+    "STREAM_FCC",
+    "STREAM_INIT",
+    "STREAM_RECALL",
     "uniform_recall_sample",
     "validate_simplex_points",
+    "verify_total_order",
 ]

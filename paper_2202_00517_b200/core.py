@@ -8,7 +8,7 @@ device kernels implement.
 from __future__ import annotations
 
 from abc import ABC, abstractmethod
-from typing import Generic, Iterator, Sequence, TypeVar
+from typing import Generic, Iterable, Iterator, Mapping, Sequence, TypeVar
 
 import numpy as np
 
@@ -77,3 +77,31 @@ class ScoredRankingSystem(RankingSystem):
         if x == y or x == z or y == z:
             raise ValueError(f"compare needs pairwise distinct ids, got ({x}, {y}, {z})")
         return -1 if (self.score(x, y), y) < (self.score(x, z), z) else 1
+
+
+def build_cofriends(friends: Mapping[ItemId, Iterable[ItemId]]) -> dict[ItemId, set[ItemId]]:
+    """core.py:196-206 — transpose a friends digraph given as a mapping: y in
+    friends[x] iff x in cofriends[y]; every input key appears, possibly empty.
+    (The device path builds the same transpose as a CSR, knnd_csr_build.)"""
+    cofriends: dict[ItemId, set[ItemId]] = {x: set() for x in friends}
+    for x, targets in friends.items():
+        for y in targets:
+            cofriends.setdefault(y, set()).add(x)
+    return cofriends
+
+
+def verify_total_order(rs: RankingSystem, anchor: ItemId, ids: Sequence[ItemId]) -> bool:
+    """core.py:209-235 — exhaustive anti-symmetry and transitivity check of the
+    anchor's order over `ids` (O(m^3); a desk-scale diagnostic)."""
+    others = [i for i in ids if i != anchor]
+    for y in others:
+        for z in others:
+            if y < z and (rs.compare(anchor, y, z) < 0) == (rs.compare(anchor, z, y) < 0):
+                return False
+    for y in others:
+        for z in others:
+            for w in others:
+                if len({y, z, w}) == 3 and rs.compare(anchor, y, z) < 0 and rs.compare(anchor, z, w) < 0 \
+                        and not rs.compare(anchor, y, w) < 0:
+                    return False
+    return True

@@ -398,6 +398,21 @@ def friend_clustering_rate(state: KnnState, sample_count: int, rng: np.random.Ge
     return cnt / sample_count
 
 
+def candidate_set(x: ItemId, state: KnnState) -> np.ndarray:
+    """descent.py:216-227 — x's new acquaintances: cofriends, friends of friends
+    and friends of cofriends, unique and sorted by id, without x and without
+    x's current friends (the comparator engine's candidate set; the device
+    join ranks the superset that keeps the friends, descent.py:230-242)."""
+    _check_state(state)
+    friends = state.friends
+    frs = friends[x]
+    cof = state.cofriends_of(x)
+    cand = np.unique(np.concatenate((cof, friends[frs].ravel(), friends[cof].ravel())))
+    mask = cand != x
+    mask &= ~np.isin(cand, frs)
+    return cand[mask]
+
+
 def propose_new_friend_set(x: ItemId, state: KnnState, rs) -> np.ndarray:
     """descent.py:252-259 — the K best of x's friends and candidates, best first."""
     _check_state(state)

@@ -43,6 +43,18 @@ def validate_simplex_points(points, tol: float = 1e-12) -> None:
         raise ValueError(f"simplex rows must sum to 1 within {tol}, worst error {err:.3e}")
 
 
+def kl_divergence(x, y) -> float:
+    """similarity.py:36-47 — KL divergence of y from x in nats, sum x_i log(x_i / y_i),
+    for one pair of host vectors (the batched device form is KlRankingSystem.batch_scores)."""
+    x = np.asarray(x, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64)
+    if x.shape != y.shape:
+        raise ValueError(f"dimension mismatch: {x.shape} vs {y.shape}")
+    if not ((x > 0.0).all() and (y > 0.0).all()):
+        raise ValueError("coordinates must be strictly positive")
+    return float(np.sum(x * np.log(x / y)))
+
+
 def sample_simplex_uniform(d: int, n: int, rng, concentration: float = 1.0) -> np.ndarray:
     """similarity.py:50-77: n i.i.d. points of the open simplex in R^d."""
     if d < 2:

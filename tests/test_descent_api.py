@@ -234,3 +234,35 @@ def test_repeated_runs_on_one_ranking_system_agree(cuda, n, d, k):
     fc, hc = b2.run(ds, b2.KlRankingSystem(pts, validate=False), cfg)
     assert np.array_equal(fa, fb) and np.array_equal(fa, fc)
     assert hist(ha) == hist(hb) == hist(hc)
+
+
+# ---------------------------------------------------------------------------
+# candidate_set / propose_new_friend_set (descent.py:216-259)
+
+
+def test_candidate_set_hand_traces(cuda):
+    st = b2.KnnState(np.array([[1, 2], [0, 2], [0, 1]]))
+    assert all(b2.candidate_set(x, st).size == 0 for x in range(3))  # saturated triangle
+    assert list(b2.candidate_set(0, b2.KnnState(np.array([[1], [2], [0]])))) == [2]  # three-cycle, K = 1
+
+
+def test_candidate_set_exclusion_and_size_bound(cuda):
+    ds, rs = kl_instance(400, 4, 8)
+    k = 5
+    st = b2.init_random_kout(ds, rs, b2.DescentConfig(k=k), b2.derive_rng(8, 2))
+    for x in range(0, 400, 13):
+        cand = b2.candidate_set(x, st)
+        assert x not in cand and not np.isin(cand, st.friends[x]).any()
+        assert len(set(map(int, cand))) == cand.size and np.all(np.diff(cand) > 0)
+        cofs = st.cofriends_of(x).size
+        assert cand.size <= cofs + k * k + cofs * k
+
+
+def test_propose_matches_exhaustive_union_sort(cuda):
+    """The device join for one anchor equals sorting friends | candidates by (score, id)."""
+    ds, rs = euclid_instance(20, 1, 9)
+    st = b2.init_random_kout(ds, rs, b2.DescentConfig(k=2), b2.derive_rng(9, 2))
+    for x in range(20):
+        union = set(map(int, st.friends[x])) | set(map(int, b2.candidate_set(x, st)))
+        expected = sorted(union, key=lambda y: (rs.score(x, y), y))[:2]
+        assert list(b2.propose_new_friend_set(x, st, rs)) == expected

@@ -125,3 +125,56 @@ def test_golden_init_is_reachable_from_host_draws(small_meta, small_tables):
         pts = b2.sample_simplex_uniform(meta["d"], meta["n"], b2.derive_rng(meta["seed"], 1, meta["d"]))
         draws = b2.random_kout_draws(meta["n"], meta["k"], b2.derive_rng(meta["seed"], 2))
         assert sha_i32(native.sort_rows(native.Tables(pts), draws)) == meta["init_sha"]
+
+
+# ---------------------------------------------------------------------------
+# host helpers of the API (similarity.py:36-47, core.py:196-235)
+
+
+def test_kl_divergence_helper():
+    from scipy.special import rel_entr
+
+    x, y = np.array([0.5, 0.5]), np.array([0.25, 0.75])
+    assert b2.kl_divergence(x, y) == pytest.approx(0.143841, abs=1e-6)
+    assert b2.kl_divergence(y, x) == pytest.approx(0.130812, abs=1e-6)
+    assert b2.kl_divergence(x, x) == 0.0
+    rng = np.random.default_rng(1)
+    for _ in range(20):
+        e = rng.standard_exponential((2, 8))
+        p, q = e / e.sum(axis=1, keepdims=True)
+        assert b2.kl_divergence(p, q) == pytest.approx(float(rel_entr(p, q).sum()), rel=1e-12)
+    with pytest.raises(ValueError):
+        b2.kl_divergence(np.array([0.5, 0.5]), np.array([0.2, 0.3, 0.5]))
+    with pytest.raises(ValueError):
+        b2.kl_divergence(np.array([0.0, 1.0]), np.array([0.5, 0.5]))
+
+
+def test_build_cofriends():
+    assert b2.build_cofriends({0: {1}, 1: {0}}) == {0: {1}, 1: {0}}
+    assert b2.build_cofriends({0: {1}, 1: {2}, 2: {0}}) == {1: {0}, 2: {1}, 0: {2}}
+    rng = np.random.default_rng(7)
+    friends = {x: set(map(int, (lambda r: r + (r >= x))(rng.permutation(99)[:5]))) for x in range(100)}
+    cof = b2.build_cofriends(friends)
+    for y in range(100):
+        assert cof[y] == {x for x in range(100) if y in friends[x]}
+
+
+class _LineRanking(b2.RankingSystem):
+    """Points on a line ranked by distance, ties by id (host-only, for the checker)."""
+
+    def __init__(self, pos):
+        self.pos = pos
+
+    def compare(self, x, y, z):
+        return -1 if (abs(self.pos[y] - self.pos[x]), y) < (abs(self.pos[z] - self.pos[x]), z) else 1
+
+
+class _Cyclic(b2.RankingSystem):
+    def compare(self, x, y, z):  # y < z iff (z - y) mod 3 == 1: intransitive on {0, 1, 2}
+        return -1 if (z - y) % 3 == 1 else 1
+
+
+def test_verify_total_order():
+    rs = _LineRanking([0.0, 1.0, -1.0, 3.0, 2.5])
+    assert b2.verify_total_order(rs, 0, range(5))
+    assert not b2.verify_total_order(_Cyclic(), 5, [0, 1, 2])
