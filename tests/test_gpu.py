@@ -225,10 +225,13 @@ def _hub_table(n, k, hubs, rng):
     return t
 
 
-@pytest.mark.parametrize("n,d,k", [(20000, 5, 10), (30000, 20, 20), (12000, 50, 30), (6000, 8, 64)])
+@pytest.mark.parametrize("n,d,k", [(20000, 5, 10), (30000, 20, 20), (12000, 50, 30), (6000, 8, 64), (15000, 16, 16),
+                                   (9000, 7, 12)])
 def test_size_classes_and_hubs_vs_oracle(cuda, n, d, k):
     """Anchors spread over all three size classes (warp-block smem, large smem,
-    global-table hubs) give exactly the oracle's rows and |U|."""
+    global-table hubs) give exactly the oracle's rows and |U|; the shapes cover
+    the compile-time row widths and the generic one (d = 16: ld 16; d = 7: ld 8),
+    and K % 4 == 0 (int4 friend rows) as well as K % 4 != 0."""
     rng = np.random.default_rng(n + d + k)
     pts = port.experiment_points(n, d, 3)
     hubs = [(7, n // 4), (11, n // 10), (13, 40 * k), (17, 8 * k), (19, 3 * k), (23, 2 * k)]
