@@ -619,6 +619,8 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
   }
   __syncthreads();
   if (hdr[8] < count) prefetch(0, hdr[9], hdr64[0], hdr[12]);
+  cp_async_wait_all();
+  __syncthreads();  // the first anchor's inputs are in buffer 0
   int pb = 0;
 
   for (int a = hdr[8]; a < count; a = hdr[8]) {
@@ -646,8 +648,9 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
       Ha = 1 << la;
       sha = 32u - (unsigned)la;
     }
-    cp_async_wait_all();
-    __syncthreads();  // this anchor's inputs are in buffer pb; everyone has read hdr[8..12]
+    // (this anchor's inputs are in buffer pb: the end of the previous anchor
+    // waited for them before its barrier; hdr[8..12] is rewritten only after
+    // the phase-0 barrier below)
 
     // ---- phase 0: clear table + histograms (S and the anchor rows were prefetched)
     {
@@ -976,6 +979,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
         if (p.out_ucount) p.out_ucount[xr] = U;
       }
     }
+    cp_async_wait_all();  // the next anchor's inputs (prefetched into the other buffer)
     __syncthreads();
     pb ^= 1;
   }
