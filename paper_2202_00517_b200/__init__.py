@@ -58,7 +58,11 @@ from .similarity import (
     KlRankingSystem,
     euclidean_ranking,
     kl_divergence,
+    load_points_csv,
+    load_points_f64,
     sample_simplex_uniform,
+    save_points_csv,
+    save_points_f64,
     validate_simplex_points,
 )
 
@@ -89,6 +93,10 @@ __all__ = [
     "init_random_kout",
     "ItemId",
     "kl_divergence",
+    "load_points_csv",
+    "load_points_f64",
+    "save_points_csv",
+    "save_points_f64",
     "KlRankingSystem",
     "KnndError",
     "KnnState",

@@ -338,3 +338,41 @@ def device_tables_for(rs, device=None):
         with torch.cuda.device(dev):
             cache[dev] = make(dev)
     return cache[dev]
+
+
+# ---------------------------------------------------------------------------
+# dataset files (similarity.py:173-205): the CLI's --data-in / --data-out
+
+_F64_HEAD = np.dtype([("d", "<u4"), ("n", "<u4")])  # 8-byte little-endian (d, n)
+
+
+def save_points_csv(path, points) -> None:
+    """similarity.py:176-178 — one point per line, d columns, %.17g (round-trips fp64)."""
+    np.savetxt(path, _as_points(points), delimiter=",", fmt="%.17g")
+
+
+def load_points_csv(path) -> np.ndarray:
+    """similarity.py:181-183."""
+    return np.loadtxt(path, delimiter=",", dtype=np.float64, ndmin=2)
+
+
+def save_points_f64(path, points) -> None:
+    """similarity.py:186-192 — header (d, n) as two uint32, then row-major <f8."""
+    pts = np.ascontiguousarray(_as_points(points), dtype="<f8")
+    head = np.array([(pts.shape[1], pts.shape[0])], dtype=_F64_HEAD)
+    with open(path, "wb") as fh:
+        fh.write(head.tobytes())
+        fh.write(pts.tobytes())
+
+
+def load_points_f64(path) -> np.ndarray:
+    """similarity.py:195-205 — same errors for a short header or payload."""
+    raw = open(path, "rb").read()
+    if len(raw) < _F64_HEAD.itemsize:
+        raise ValueError(f"truncated header in {path}")
+    head = np.frombuffer(raw[:_F64_HEAD.itemsize], dtype=_F64_HEAD)[0]
+    d, n = int(head["d"]), int(head["n"])
+    got = len(raw) - _F64_HEAD.itemsize
+    if got != n * d * 8:
+        raise ValueError(f"expected {n * d * 8} payload bytes in {path}, found {got}")
+    return np.frombuffer(raw, dtype="<f8", offset=_F64_HEAD.itemsize).reshape(n, d).copy()
