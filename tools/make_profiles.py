@@ -2,6 +2,7 @@
 
   profiles/<tag>_bench_c3.json            bench.py JSON line (B200 arm)
   profiles/<tag>_bench_reference_c3.json  bench.py --impl reference JSON line
+  profiles/<tag>_bench_c{2,4,5}.json      bench.py --config c2/c4/c5 JSON lines
   profiles/<tag>_ncu_launches_c3.json     per-launch gpu__time_duration of one bench step (ncu, cold cache)
   profiles/<tag>_ncu_join_w1_summary.txt  ncu --set full summary of one W1 local-join launch
   profiles/<tag>_ncu_join_w1_lines.txt    per-source-line stall samples / instructions of that launch
@@ -14,7 +15,8 @@ SKIP = 9  # the ncu capture's -s (W1 launches skipped)
 G = "gpurun_out"
 P = "profiles"
 os.makedirs(P, exist_ok=True)
-for src, dst in (("bench.log", "bench_c3.json"), ("bench_ref.log", "bench_reference_c3.json")):
+for src, dst in (("bench.log", "bench_c3.json"), ("bench_ref.log", "bench_reference_c3.json"),
+                 ("bench_c2.log", "bench_c2.json"), ("bench_c4.log", "bench_c4.json"), ("bench_c5.log", "bench_c5.json")):
     p = os.path.join(G, src)
     if os.path.exists(p):
         line = open(p).readline().strip()
