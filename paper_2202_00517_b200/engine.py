@@ -234,6 +234,13 @@ class Engine:
             except Exception as exc:  # e.g. no P2P / IPC between these devices
                 print(f"knnd: fused peer exchange unavailable ({type(exc).__name__}: {exc}); "
                       "using the NCCL all-gather", file=sys.stderr)
+            # every rank must take the same exchange, or the rounds deadlock
+            ok = torch.tensor([int(self.peer is not None)], dtype=torch.int32, device=self.device)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=self.group)
+            if int(ok.item()) == 0 and self.peer is not None:
+                print("knnd: another rank could not map the peer tables; using the NCCL all-gather",
+                      file=sys.stderr)
+                self.peer = None
         return self.peer is not None
 
     # -- tables -----------------------------------------------------------

@@ -96,3 +96,34 @@ def test_fused_peer_exchange_matches_reference(small_meta, world):
     for rank in range(world):
         assert res[rank]["hist"] == expect, rank
         assert res[rank]["sha"] == meta["rounds"][-1]["sha"], rank
+
+
+def _consensus_worker(rank, world, port, out):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2202_00517_b200 import engine as E
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        def mapped(eng):  # rank 1 cannot map the peer tables, rank 0 can
+            if eng.shard.rank == 1:
+                raise RuntimeError("no peer access")
+            return E.PeerTables([eng.alloc_table(), eng.alloc_table()], [[], []], lambda i: None)
+
+        E.exchange_mode = lambda eng: "peer"
+        E.symmetric_peer_tables = mapped
+        eng = E.Engine(100, 4, torch.device("cpu"), ops=object())
+        out[rank] = (eng.enable_peer_exchange(), eng.peer is None)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_exchange_fallback_is_collective():
+    """If any rank fails to map the symmetric tables, every rank falls back to
+    the all-gather (mixed exchanges would deadlock the rounds)."""
+    out = mp.Manager().dict()
+    mp.spawn(_consensus_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    assert dict(out) == {0: (False, True), 1: (False, True)}
