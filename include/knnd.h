@@ -4,9 +4,14 @@
  *
  * One shared object, libknnd.so, built for sm_100a.  Every entry point takes
  * plain device pointers, sizes and a CUDA stream (passed as void*), is
- * stream-ordered, allocates nothing and keeps no state apart from a per-thread
- * last-error string and a launch counter.  The caller (the Python host in
+ * stream-ordered, allocates no device memory and keeps no state apart from a
+ * per-thread last-error string and a launch counter: streams are the
+ * caller's, and the only CUDA objects the library creates are the two fork /
+ * join events of one *_local_join_peers call with a side stream, destroyed
+ * before that call returns.  The caller (the Python host in
  * paper_2202_00517_b200/, using PyTorch for device buffers) owns all memory.
+ * Environment variables read per call (diagnostics / A-B only; results never
+ * depend on them): KNND_PLAN, KNND_SIDE_CLASSES, KNND_CLASS_TIMING.
  *
  * Return value: KNND_OK (0) or a negative KNND_E* code; knnd_last_error()
  * then describes the failure.  Errors never fall back to a CPU path.
@@ -26,7 +31,7 @@
 extern "C" {
 #endif
 
-#define KNND_ABI_VERSION 1
+#define KNND_ABI_VERSION 2
 
 enum {
   KNND_OK = 0,
@@ -129,6 +134,11 @@ int knnd_local_join(const double *points, const float *log32, const double *log6
  * memory over NVLink).  The stores overlap the join; before any rank reads the
  * gathered table, the caller runs a cross-rank barrier on the stream (the
  * kernels end with a system-scope fence).  npeers in 0..KNND_MAX_PEERS.
+ * side_stream (nullable, a stream of the same device other than `stream`):
+ * the few long anchors of the big-table size classes run there, concurrently
+ * with the bulk classes on `stream`; the call forks to it and joins back, so
+ * all of its work is ordered before later work on `stream`.  NULL runs every
+ * class on `stream` (knnd_local_join does that).  Results do not depend on it.
  */
 int knnd_local_join_peers(const double *points, const float *log32, const double *log64,
                           const double *xlogx, int64_t n, int32_t d, int32_t ld32,
@@ -138,7 +148,7 @@ int knnd_local_join_peers(const double *points, const float *log32, const double
                           int32_t *out_ucount, unsigned long long *tally,
                           const float *bound_in, float *bound_out, void *ws, size_t ws_bytes,
                           uint32_t flags, int32_t *const *peer_tables, int32_t npeers,
-                          void *stream);
+                          void *stream, void *side_stream);
 
 /*
  * Friend clustering rate count — friend_clustering_rate (descent.py:317-338)
@@ -227,7 +237,7 @@ int knnd_l2_local_join(const float *anchor32, const float *cand32, const double 
                        int32_t *out_ids, double *out_d2, int32_t *out_ucount,
                        unsigned long long *tally, const float *bound_in, float *bound_out, void *ws,
                        size_t ws_bytes, void *stream);
-/* knnd_l2_local_join with the fused table exchange of knnd_local_join_peers */
+/* knnd_l2_local_join with the fused table exchange (and side stream) of knnd_local_join_peers */
 int knnd_l2_local_join_peers(const float *anchor32, const float *cand32, const double *rows64,
                              const double *sq64, int64_t n, int32_t d, int32_t ld32,
                              double maxnorm, const int32_t *friends, int32_t k,
@@ -235,7 +245,8 @@ int knnd_l2_local_join_peers(const float *anchor32, const float *cand32, const d
                              int64_t row_hi, int32_t max_indeg, int32_t *out_ids, double *out_d2,
                              int32_t *out_ucount, unsigned long long *tally,
                              const float *bound_in, float *bound_out, void *ws, size_t ws_bytes,
-                             int32_t *const *peer_tables, int32_t npeers, void *stream);
+                             int32_t *const *peer_tables, int32_t npeers, void *stream,
+                             void *side_stream);
 int knnd_l2_exact_knn(const float *anchor32, const float *cand32, const double *rows64,
                       const double *sq64, int64_t n, int32_t d, int32_t ld32, double maxnorm,
                       const int32_t *queries, int64_t nq, int32_t k, int32_t cap, int32_t *out_ids,

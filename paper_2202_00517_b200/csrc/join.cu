@@ -1042,20 +1042,19 @@ __device__ __forceinline__ void prefetch_anchor(const JoinParams &p, int x, int6
   cp_async_commit();
 }
 
-template <int NV4, int KPL, bool GLIST, bool VF>
-__global__ void __launch_bounds__(128, GLIST ? 6 : 4)
+template <int NV4, int KPL, bool VF>
+__global__ void __launch_bounds__(128, 4)
     join_warp_kernel(JoinParams p, const int32_t *__restrict__ alist, const int32_t *__restrict__ acount, int logH,
-                     int SW, int32_t *__restrict__ glists) {
+                     int SW) {
   constexpr int Q = 2 * KPL;  // per-lane kept screened values
   extern __shared__ __align__(16) unsigned char sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int H = 1 << logH;
   const unsigned shift = 32u - (unsigned)logH;
   const WarpSlab L = warp_slab(p.d, p.ld, H, SW);
-  unsigned char *base = sm + (size_t)warp * (GLIST ? L.list : L.total);  // GLIST: no list in smem
+  unsigned char *base = sm + (size_t)warp * L.total;
   int32_t *table = reinterpret_cast<int32_t *>(base + L.table);
-  int32_t *list = GLIST ? glists + (size_t)(blockIdx.x * (blockDim.x >> 5) + warp) * (H >> 1)
-                        : reinterpret_cast<int32_t *>(base + L.list);
+  int32_t *list = reinterpret_cast<int32_t *>(base + L.list);
   float *scores = reinterpret_cast<float *>(table);            // phase 2-3: [0, U)
   double *stage64 = reinterpret_cast<double *>(table);         // phase 4: whole table
   const int K = p.K, K1 = K + 1;
@@ -1412,8 +1411,7 @@ __global__ void classify_kernel(const int64_t *__restrict__ indptr, int64_t m, i
 // ---------------------------------------------------------------------------
 // host side: the size-class plan
 
-enum { KIND_WARP = 0, KIND_BLOCK128 = 1, KIND_BLOCK256 = 2, KIND_GLOBAL = 3, KIND_BLOCK64 = 4, KIND_WARPG = 5,
-       KIND_BLOCK512 = 6 };
+enum { KIND_WARP = 0, KIND_BLOCK128 = 1, KIND_BLOCK256 = 2, KIND_GLOBAL = 3, KIND_BLOCK512 = 4 };
 
 struct Cls {
   int kind, logH, sw;
@@ -1426,8 +1424,7 @@ struct Plan {
   Cls c[MAXCLS];
   int nslab;
   int64_t slab_ints;
-  int64_t glist_ints;  // per-warp global unique lists (KIND_WARPG)
-  size_t lists_off, counts_off, slab_off, glist_off, total;
+  size_t lists_off, counts_off, slab_off, total;
 };
 
 constexpr int WARP_BLOCK = 128, GL = 512;
@@ -1448,12 +1445,6 @@ static int parse_plan(const char *spec, int kind[], int logH[]) {
     if (q[0] == 'w') {
       k = KIND_WARP;
       l = atoi(q + 1);
-    } else if (q[0] == 'g') {
-      k = KIND_WARPG;
-      l = atoi(q + 1);
-    } else if (q[0] == 'b' && !strncmp(q + 1, "64:", 3)) {
-      k = KIND_BLOCK64;
-      l = atoi(q + 4);
     } else if (q[0] == 'b' && !strncmp(q + 1, "128:", 4)) {
       k = KIND_BLOCK128;
       l = atoi(q + 5);
@@ -1477,7 +1468,9 @@ static int parse_plan(const char *spec, int kind[], int logH[]) {
   return n;
 }
 
-static Plan make_plan(int64_t m, int d, int K, int max_indeg) {
+constexpr int64_t HUB_SLAB_BUDGET = (int64_t)4 << 30;
+
+static Plan make_plan(int64_t n_items, int64_t m, int d, int K, int max_indeg) {
   Plan P{};
   P.kpl = K <= 32 ? 1 : 2;
   P.nv4 = (d + 3) / 4;
@@ -1529,14 +1522,24 @@ static Plan make_plan(int64_t m, int d, int K, int max_indeg) {
   g.logH = g.need ? ilog2_ceil(2 * Pmax) : 0;
   g.sw = (K + max_indeg + 31) & ~31;  // keeps the table int4-aligned in the slab
   P.ncls = n + 1;
-  P.nslab = g.need ? 2 * num_sms() : 0;
   P.slab_ints = g.need ? (int64_t)align_up((size_t)g.sw + ((size_t)3 << g.logH) / 2, 64) : 0;
-  P.glist_ints = 0;
-  for (int i = 0; i < n; ++i)
-    if (P.c[i].kind == KIND_WARPG && P.c[i].need) {
-      const int64_t per = (int64_t)num_sms() * 64 * (((int64_t)1 << P.c[i].logH) / 2);  // <= 64 warps per SM
-      if (per > P.glist_ints) P.glist_ints = per;
-    }
+  // hub slabs: one per resident block (2 per SM), but no more than the anchors
+  // the class can hold — its in-degrees exceed cmin and they sum to at most
+  // n*K — and at most HUB_SLAB_BUDGET bytes in all (at least one slab): every
+  // slab is sized for the largest hub, so skewed in-degrees (duplicate points,
+  // hubness) would otherwise ask for tens of GB.  Fewer slabs only means fewer
+  // hub blocks in flight (the class kernel's grid is capped at nslab).
+  P.nslab = 0;
+  if (g.need) {
+    int64_t ns = 2 * (int64_t)num_sms();
+    const int64_t cmin = prev / K1 - K;  // the global class: (K + c)(K + 1) > prev, so c > cmin
+    const int64_t hubs = cmin >= 0 ? (n_items * K) / (cmin + 1) : m;
+    if (ns > hubs) ns = hubs;
+    if (ns > m) ns = m;
+    const int64_t by_budget = HUB_SLAB_BUDGET / (P.slab_ints * 4);
+    if (ns > by_budget) ns = by_budget;
+    P.nslab = (int)(ns < 1 ? 1 : ns);
+  }
   size_t o = 0;
   P.lists_off = o;
   o = align_up(o + (size_t)P.ncls * m * 4, 256);
@@ -1544,8 +1547,6 @@ static Plan make_plan(int64_t m, int d, int K, int max_indeg) {
   o = align_up(o + 64, 256);
   P.slab_off = o;
   o = align_up(o + (size_t)P.nslab * P.slab_ints * 4, 256);
-  P.glist_off = o;
-  o = align_up(o + (size_t)P.glist_ints * 4, 256);
   P.total = o;
   return P;
 }
@@ -1576,13 +1577,12 @@ static int launch_join(const JoinParams &p, const int32_t *alist, const int32_t 
   return KNND_OK;
 }
 
-template <int NV4, int KPL, bool GLIST>
+template <int NV4, int KPL>
 static int launch_warp(const JoinParams &p, const int32_t *alist, const int32_t *acount, int logH, int SW,
-                       int32_t *glists, cudaStream_t st) {
+                       cudaStream_t st) {
   // friend rows as int4 when they are 16-B aligned (K % 4 == 0)
-  auto kern = (p.K % 4 == 0) ? join_warp_kernel<NV4, KPL, GLIST, true> : join_warp_kernel<NV4, KPL, GLIST, false>;
-  WarpSlab L = warp_slab(p.d, p.ld, 1 << logH, SW);
-  if (GLIST) L.total = L.list;  // the unique list lives in the global slab
+  auto kern = (p.K % 4 == 0) ? join_warp_kernel<NV4, KPL, true> : join_warp_kernel<NV4, KPL, false>;
+  const WarpSlab L = warp_slab(p.d, p.ld, 1 << logH, SW);
   // warps per block: the largest of 4/2/1 that keeps the most warps resident
   // (big tables leave room for fewer than 4 slabs per block slot)
   int best_wpb = 0, best_warps = 0;
@@ -1593,7 +1593,6 @@ static int launch_warp(const JoinParams &p, const int32_t *alist, const int32_t 
     KNND_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_b));
     int per_sm = 0;
     KNND_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpb * 32, sm_b));
-    if (GLIST && per_sm * wpb > 64) per_sm = 64 / wpb;  // the workspace holds 64 warp lists per SM
     if (per_sm * wpb > best_warps) {
       best_warps = per_sm * wpb;
       best_wpb = wpb;
@@ -1605,7 +1604,7 @@ static int launch_warp(const JoinParams &p, const int32_t *alist, const int32_t 
     return KNND_EUNSUPPORTED;
   }
   KNND_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<(best_warps / best_wpb) * num_sms(), best_wpb * 32, smem, st>>>(p, alist, acount, logH, SW, glists);
+  kern<<<(best_warps / best_wpb) * num_sms(), best_wpb * 32, smem, st>>>(p, alist, acount, logH, SW);
   KNND_LAUNCHED(1);
   return KNND_OK;
 }
@@ -1630,28 +1629,23 @@ static int dispatch_block(const Plan &P, const JoinParams &p, const int32_t *ali
 #undef KNND_CALL
 }
 
-template <bool GLIST>
 static int dispatch_warp(const Plan &P, const JoinParams &p, const int32_t *alist, const int32_t *acount, int logH,
-                         int SW, int32_t *glists, cudaStream_t st) {
-#define KNND_CALL(NV)                                                                     \
-  return P.kpl == 1 ? launch_warp<NV, 1, GLIST>(p, alist, acount, logH, SW, glists, st) \
-                    : launch_warp<NV, 2, GLIST>(p, alist, acount, logH, SW, glists, st)
+                         int SW, cudaStream_t st) {
+#define KNND_CALL(NV)                                                             \
+  return P.kpl == 1 ? launch_warp<NV, 1>(p, alist, acount, logH, SW, st) \
+                    : launch_warp<NV, 2>(p, alist, acount, logH, SW, st)
   KNND_NV_SWITCH(KNND_CALL)
 #undef KNND_CALL
 }
 
 static int dispatch_class(const Plan &P, int i, const JoinParams &p, const int32_t *lists, const int32_t *counts,
-                          int64_t m, int32_t *slabs, int32_t *glists, cudaStream_t st) {
+                          int64_t m, int32_t *slabs, cudaStream_t st) {
   const Cls &c = P.c[i];
   const int32_t *alist = lists + (int64_t)i * m;
   const int32_t *acount = counts + i;
   switch (c.kind) {
     case KIND_WARP:
-      return dispatch_warp<false>(P, p, alist, acount, c.logH, c.sw, nullptr, st);
-    case KIND_WARPG:
-      return dispatch_warp<true>(P, p, alist, acount, c.logH, c.sw, glists, st);
-    case KIND_BLOCK64:
-      return dispatch_block<64, false>(P, p, alist, acount, c.logH, c.sw, nullptr, 0, 0, st);
+      return dispatch_warp(P, p, alist, acount, c.logH, c.sw, st);
     case KIND_BLOCK128:
       return dispatch_block<128, false>(P, p, alist, acount, c.logH, c.sw, nullptr, 0, 0, st);
     case KIND_BLOCK256:
@@ -1671,9 +1665,8 @@ extern "C" {
 
 size_t knnd_local_join_workspace_bytes(int64_t n, int32_t d, int32_t k, int64_t row_lo, int64_t row_hi,
                                        int32_t max_indeg) {
-  (void)n;
-  if (k < 2 || k > 64 || d < 1 || row_hi < row_lo || max_indeg < 0) return 0;
-  return make_plan(row_hi - row_lo, d, k, max_indeg).total;
+  if (k < 2 || k > 64 || d < 1 || row_hi < row_lo || max_indeg < 0 || n < 1) return 0;
+  return make_plan(n, row_hi - row_lo, d, k, max_indeg).total;
 }
 
 }  // extern "C"
@@ -1681,7 +1674,8 @@ size_t knnd_local_join_workspace_bytes(int64_t n, int32_t d, int32_t k, int64_t 
 // shared by the KL and L2 entries: validation that does not depend on the
 // metric, the plan, and the class launches
 static int join_run(const char *who, JoinParams &p, int64_t n, int32_t dplan, int32_t k, int64_t row_lo,
-                    int64_t row_hi, int32_t max_indeg, void *ws, size_t ws_bytes, void *stream) {
+                    int64_t row_hi, int32_t max_indeg, void *ws, size_t ws_bytes, void *stream,
+                    void *side_stream) {
   const int32_t d = p.d, ld32 = p.ld;
   KNND_CHECK_ARG(p.F && p.indptr && p.indices && p.out_ids && p.tally, "%s: null pointer", who);
   KNND_CHECK_ARG(n >= 2 && d >= 1, "%s: bad shape n=%lld d=%d", who, (long long)n, d);
@@ -1699,7 +1693,7 @@ static int join_run(const char *who, JoinParams &p, int64_t n, int32_t dplan, in
     set_error("%s: pre-dedup bound (K+%d)(K+1) too large", who, max_indeg);
     return KNND_EUNSUPPORTED;
   }
-  const Plan P = make_plan(m, dplan, k, max_indeg);
+  const Plan P = make_plan(n, m, dplan, k, max_indeg);
   if (ws_bytes < P.total || !ws) {
     set_error("%s: workspace %zu < %zu bytes", who, ws_bytes, P.total);
     return KNND_EWORKSPACE;
@@ -1709,7 +1703,6 @@ static int join_run(const char *who, JoinParams &p, int64_t n, int32_t dplan, in
   int32_t *lists = reinterpret_cast<int32_t *>(w + P.lists_off);
   int32_t *counts = reinterpret_cast<int32_t *>(w + P.counts_off);
   int32_t *slabs = reinterpret_cast<int32_t *>(w + P.slab_off);
-  int32_t *glists = reinterpret_cast<int32_t *>(w + P.glist_off);
   const int64_t *indptr = p.indptr;
   unsigned long long *tally = p.tally;
   p.lo = row_lo;
@@ -1729,50 +1722,51 @@ static int join_run(const char *who, JoinParams &p, int64_t n, int32_t dplan, in
   }
   // diagnostics: KNND_CLASS_TIMING=1 times each class (synchronising) and prints
   // anchors / comparisons / ms per class to stderr
-  static const bool timing = getenv("KNND_CLASS_TIMING") != nullptr;
-  // The big-table classes (>= 2^14 slots and the hubs) run on a side stream,
-  // concurrently with the rest: they hold few anchors, each long and latency
-  // bound, and serialised their tails left most SMs idle — ~0.1-0.3 ms per
-  // round, a 10-15% loss once a rank holds 1/8 of the anchors.  Persistent
-  // blocks that find no anchor exit at once, so the other classes fill the
-  // machine around the busy ones.  Measured (C3): P = 1 +0.5%, the 8-rank
-  // projection's join -5.5%; C4 -0.7%.  KNND_SIDE_CLASSES=k overrides (the k
-  // biggest classes; 0 = all serial).  One side stream and two events per host
-  // thread and device, created on first use.
-  static const int nside_env = getenv("KNND_SIDE_CLASSES") ? atoi(getenv("KNND_SIDE_CLASSES")) : -1;
+  const bool timing = getenv("KNND_CLASS_TIMING") != nullptr;
+  // The big-table classes (>= 2^14 slots and the hubs) run on the caller's
+  // side stream (when one is given), concurrently with the rest: they hold few
+  // anchors, each long and latency bound, and serialised their tails left most
+  // SMs idle — ~0.1-0.3 ms per round, a 10-15% loss once a rank holds 1/8 of
+  // the anchors.  Persistent blocks that find no anchor exit at once, so the
+  // other classes fill the machine around the busy ones.  Measured (C3): P = 1
+  // +0.5%, the 8-rank projection's join -5.5%; C4 -0.7%.  KNND_SIDE_CLASSES=k
+  // overrides (the k biggest classes; 0 = all serial).  The fork / join events
+  // live for this call only (destroyed here; CUDA releases them once they
+  // complete), so the library keeps no stream or event state.
+  const char *nside_s = getenv("KNND_SIDE_CLASSES");
+  const int nside_env = nside_s ? atoi(nside_s) : -1;
   int ig = P.ncls;  // classes [ig, ncls) go to the side stream
   if (nside_env >= 0) {
     ig = P.ncls - nside_env;
   } else {
     while (ig - 1 > 0 && (P.c[ig - 1].kind == KIND_GLOBAL || P.c[ig - 1].logH >= 14)) --ig;
   }
-  const bool side = !timing && ig > 0 && ig < P.ncls;
-  cudaEvent_t ev_join = nullptr;
+  cudaStream_t sst = as_stream(side_stream);
+  const bool side = sst != nullptr && sst != st && !timing && ig > 0 && ig < P.ncls;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   if (side) {
-    struct Side {
-      int dev = -1;
-      cudaStream_t s = nullptr;
-      cudaEvent_t fork = nullptr, join = nullptr;
-    };
-    static thread_local Side sides[16];
-    int dev = 0;
-    KNND_CUDA(cudaGetDevice(&dev));
-    Side &sd = sides[dev & 15];
-    if (sd.dev != dev || !sd.s) {
-      KNND_CUDA(cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking));
-      KNND_CUDA(cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming));
-      KNND_CUDA(cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming));
-      sd.dev = dev;
+    KNND_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    if (cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventDestroy(ev_fork);
+      set_error("%s: cudaEventCreate failed", who);
+      return KNND_ECUDA;
     }
-    ev_join = sd.join;
-    KNND_CUDA(cudaEventRecord(sd.fork, st));
-    KNND_CUDA(cudaStreamWaitEvent(sd.s, sd.fork, 0));
-    for (int i = P.ncls - 1; i >= ig; --i) {
-      if (!P.c[i].need) continue;
-      const int rc = dispatch_class(P, i, p, lists, counts, m, slabs, glists, sd.s);
-      if (rc) return rc;
+    int rc = KNND_OK;
+    if (cudaEventRecord(ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(sst, ev_fork, 0) != cudaSuccess) {
+      set_error("%s: fork to the side stream failed", who);
+      rc = KNND_ECUDA;
     }
-    KNND_CUDA(cudaEventRecord(sd.join, sd.s));
+    for (int i = P.ncls - 1; i >= ig && rc == KNND_OK; --i)
+      if (P.c[i].need) rc = dispatch_class(P, i, p, lists, counts, m, slabs, sst);
+    if (rc == KNND_OK && cudaEventRecord(ev_join, sst) != cudaSuccess) {
+      set_error("%s: join of the side stream failed", who);
+      rc = KNND_ECUDA;
+    }
+    cudaEventDestroy(ev_fork);
+    if (rc != KNND_OK) {
+      cudaEventDestroy(ev_join);
+      return rc;
+    }
   }
   // biggest tables first: the few long hub anchors start early
   for (int i = P.ncls - 1; i >= 0; --i) {
@@ -1786,8 +1780,11 @@ static int join_run(const char *who, JoinParams &p, int64_t n, int32_t dplan, in
       cudaEventCreate(&e1);
       cudaEventRecord(e0, st);
     }
-    const int rc = dispatch_class(P, i, p, lists, counts, m, slabs, glists, st);
-    if (rc) return rc;
+    const int rc = dispatch_class(P, i, p, lists, counts, m, slabs, st);
+    if (rc) {
+      if (side) cudaEventDestroy(ev_join);
+      return rc;
+    }
     if (timing) {
       cudaEventRecord(e1, st);
       KNND_CUDA(cudaStreamSynchronize(st));
@@ -1804,7 +1801,11 @@ static int join_run(const char *who, JoinParams &p, int64_t n, int32_t dplan, in
       cudaEventDestroy(e1);
     }
   }
-  if (side) KNND_CUDA(cudaStreamWaitEvent(st, ev_join, 0));  // the hub rows are part of this call's output
+  if (side) {  // the hub rows are part of this call's output
+    const cudaError_t e = cudaStreamWaitEvent(st, ev_join, 0);
+    cudaEventDestroy(ev_join);
+    KNND_CUDA(e);
+  }
   return KNND_OK;
 }
 
@@ -1829,7 +1830,7 @@ int knnd_local_join_peers(const double *points, const float *log32, const double
                           int32_t max_indeg, int32_t *out_ids, double *out_kl, int32_t *out_ucount,
                           unsigned long long *tally, const float *bound_in, float *bound_out, void *ws,
                           size_t ws_bytes, uint32_t flags, int32_t *const *peer_tables, int32_t npeers,
-                          void *stream) {
+                          void *stream, void *side_stream) {
   KNND_CHECK_ARG(points && log32 && log64 && xlogx, "knnd_local_join: null pointer");
   JoinParams p{};
   p.points = points;
@@ -1853,7 +1854,7 @@ int knnd_local_join_peers(const double *points, const float *log32, const double
   p.pstride = d;
   p.aside32 = nullptr;
   if (int rc = set_peers(p, "knnd_local_join", peer_tables, npeers)) return rc;
-  return join_run("knnd_local_join", p, n, d, k, row_lo, row_hi, max_indeg, ws, ws_bytes, stream);
+  return join_run("knnd_local_join", p, n, d, k, row_lo, row_hi, max_indeg, ws, ws_bytes, stream, side_stream);
 }
 
 int knnd_local_join(const double *points, const float *log32, const double *log64, const double *xlogx, int64_t n,
@@ -1863,7 +1864,7 @@ int knnd_local_join(const double *points, const float *log32, const double *log6
                     float *bound_out, void *ws, size_t ws_bytes, uint32_t flags, void *stream) {
   return knnd_local_join_peers(points, log32, log64, xlogx, n, d, ld32, friends, k, indptr, indices, row_lo, row_hi,
                                max_indeg, out_ids, out_kl, out_ucount, tally, bound_in, bound_out, ws, ws_bytes, flags,
-                               nullptr, 0, stream);
+                               nullptr, 0, stream, nullptr);
 }
 
 int knnd_l2_local_join_peers(const float *anchor32, const float *cand32, const double *rows64, const double *sq64,
@@ -1871,7 +1872,8 @@ int knnd_l2_local_join_peers(const float *anchor32, const float *cand32, const d
                              const int64_t *indptr, const int32_t *indices, int64_t row_lo, int64_t row_hi,
                              int32_t max_indeg, int32_t *out_ids, double *out_d2, int32_t *out_ucount,
                              unsigned long long *tally, const float *bound_in, float *bound_out, void *ws,
-                             size_t ws_bytes, int32_t *const *peer_tables, int32_t npeers, void *stream) {
+                             size_t ws_bytes, int32_t *const *peer_tables, int32_t npeers, void *stream,
+                             void *side_stream) {
   KNND_CHECK_ARG(anchor32 && cand32 && rows64 && sq64, "knnd_l2_local_join: null pointer");
   JoinParams p{};
   p.points = rows64;  // the anchor's fp64 coordinates: the first d entries of its row
@@ -1896,7 +1898,8 @@ int knnd_l2_local_join_peers(const float *anchor32, const float *cand32, const d
   p.aside32 = anchor32;
   p.slack = (float)((d + 4) * 0x1p-53 * 4.0 * maxnorm * maxnorm);
   if (int rc = set_peers(p, "knnd_l2_local_join", peer_tables, npeers)) return rc;
-  return join_run("knnd_l2_local_join", p, n, d + 1, k, row_lo, row_hi, max_indeg, ws, ws_bytes, stream);
+  return join_run("knnd_l2_local_join", p, n, d + 1, k, row_lo, row_hi, max_indeg, ws, ws_bytes, stream,
+                  side_stream);
 }
 
 int knnd_l2_local_join(const float *anchor32, const float *cand32, const double *rows64, const double *sq64,
@@ -1907,7 +1910,7 @@ int knnd_l2_local_join(const float *anchor32, const float *cand32, const double 
                        void *stream) {
   return knnd_l2_local_join_peers(anchor32, cand32, rows64, sq64, n, d, ld32, maxnorm, friends, k, indptr, indices,
                                   row_lo, row_hi, max_indeg, out_ids, out_d2, out_ucount, tally, bound_in, bound_out,
-                                  ws, ws_bytes, nullptr, 0, stream);
+                                  ws, ws_bytes, nullptr, 0, stream, nullptr);
 }
 
 }  // extern "C"

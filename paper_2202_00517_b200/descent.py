@@ -43,6 +43,8 @@ STREAM_FCC = 3
 STREAM_RECALL = 4
 STREAM_WITNESS = 5
 
+MAX_K = 64  # the device join's limit (one or two 32-lane selection registers per lane)
+
 
 def derive_rng(seed: int, *path: int) -> np.random.Generator:
     """descent.py:43-45 — the per-purpose numpy substream."""
@@ -70,6 +72,8 @@ class DescentConfig:
     def __post_init__(self) -> None:
         if self.k < 2:
             raise ConfigError(f"k must be >= 2 (the stopping sampler draws friend pairs), got {self.k}")
+        if self.k > MAX_K:  # a device limit the reference does not have: refuse before any upload
+            raise ConfigError(f"k must be <= {MAX_K} on the B200 engine, got {self.k}")
         if self.fcc_sample_count < 1:
             raise ConfigError(f"fcc_sample_count must be >= 1, got {self.fcc_sample_count}")
         if self.max_rounds is not None and self.max_rounds < 1:
@@ -136,11 +140,16 @@ class KnnState:
         st = cls.__new__(cls)
         st._bind(eng, table, csr, max_indeg, round_index, tuple(hist))
         st._bound = bound
+        if eng.peer is not None:  # a ping-pong table of the fused exchange: remember its generation
+            i = eng.peer.index_of(table)
+            if i is not None:
+                st._peer_ref = (eng.peer, i, eng.peer.gen[i])
         return st
 
     def _bind(self, eng, table, csr, max_indeg, round_index, hist):
         self._engine = eng
-        self._table = table
+        self._table_t = table
+        self._peer_ref = None
         self._csr = csr
         self._max_indeg = max_indeg
         self.round = round_index
@@ -150,6 +159,22 @@ class KnnState:
         # (tables, per-row bound) from the round that produced this table; a
         # hint for the next join with the same tables, never shared or mutated
         self._bound = None
+
+    @property
+    def _table(self) -> torch.Tensor:
+        """The device table; raises if the fused exchange has since reused it
+        (the reference's KnnState is immutable: never hand out another table)."""
+        ref = self._peer_ref
+        if ref is not None and ref[0].gen[ref[1]] != ref[2]:
+            raise RuntimeError(f"the device table of this round-{self.round} KnnState was reused by a later round "
+                               "of the fused exchange; read .friends before the round after next")
+        return self._table_t
+
+    def _detach(self) -> None:
+        """Move the table into a private device copy (off the ping-pong pair)."""
+        if self._peer_ref is not None:
+            self._table_t = self._table.clone()
+            self._peer_ref = None
 
     # -- reference attributes ----------------------------------------------
     @property
@@ -428,11 +453,39 @@ def propose_new_friend_set(x: ItemId, state: KnnState, rs) -> np.ndarray:
     return out[0].cpu().numpy().astype(np.int64)
 
 
-def draw_fcc_schedule(n: int, k: int, cfg: DescentConfig, max_rounds: int) -> np.ndarray:
+def draw_fcc_schedule(n: int, k: int, cfg: DescentConfig, max_rounds: int, first: int = 1) -> np.ndarray:
     """Every round's FCC sample is a function of (seed, round) only
-    (descent.py:305), so all of them are drawn up front: (R, 3, S) int32."""
+    (descent.py:305): the samples of rounds first..max_rounds, (R, 3, S) int32."""
     return np.stack([fcc_samples(n, k, cfg.fcc_sample_count, derive_rng(cfg.seed, STREAM_FCC, r))
-                     for r in range(1, max_rounds + 1)])
+                     for r in range(first, max_rounds + 1)])
+
+
+class FccSchedule:
+    """The device copies of the rounds' FCC samples, drawn CHUNK rounds at a
+    time when a round first asks for them: the cost follows the rounds actually
+    run, not the round cap (run_to_fixed_point's cap can be large).
+    ``sched[r - 1]`` is round r's (3, S) int32 sample on the device."""
+
+    CHUNK = 4
+
+    def __init__(self, n: int, k: int, cfg: DescentConfig, max_rounds: int, device: torch.device):
+        self.n, self.k, self.cfg, self.max_rounds, self.device = n, k, cfg, max_rounds, device
+        self._chunks: dict[int, torch.Tensor] = {}
+
+    def __len__(self) -> int:
+        return self.max_rounds
+
+    def __getitem__(self, i: int) -> torch.Tensor:
+        if not 0 <= i < self.max_rounds:
+            raise IndexError(f"round {i + 1} is past the schedule's {self.max_rounds} rounds")
+        c = i // self.CHUNK
+        dev = self._chunks.get(c)
+        if dev is None:
+            first = c * self.CHUNK + 1
+            last = min(first + self.CHUNK - 1, self.max_rounds)
+            dev = _to_device(draw_fcc_schedule(self.n, self.k, self.cfg, last, first), self.device)
+            self._chunks = {c: dev}  # earlier chunks are done with
+        return dev[i - c * self.CHUNK]
 
 
 def descend_resident(eng: Engine, tabs, table: torch.Tensor, samples_dev: torch.Tensor, sample_count: int,
@@ -460,6 +513,7 @@ def descend_resident(eng: Engine, tabs, table: torch.Tensor, samples_dev: torch.
                 break
         elif len(history) >= 2 and history[-1].fcc <= history[-2].fcc:
             break
+    state._detach()  # the ping-pong tables are reused by the next descent
     return state, history
 
 
@@ -474,11 +528,11 @@ def _run_rounds(dataset: Dataset, rs, cfg: DescentConfig, max_rounds: int, stop_
     table = eng.alloc_table()
     rng = derive_rng(cfg.seed, STREAM_INIT)
     finish = device_random_kout_async(eng, n, k, rng, table) if n - 1 > 2 * k * k else None
-    smp = draw_fcc_schedule(n, k, cfg, max_rounds)
+    smp_dev = FccSchedule(n, k, cfg, max_rounds, eng.device)
+    smp_dev[0]  # the first rounds' samples are drawn while the draw kernel runs
     tabs = device_tables_for(rs, eng.device)
     if not (finish is not None and finish()):
         eng.upload_rows(random_kout_draws(n, k, rng), table)
-    smp_dev = _to_device(smp, tabs.device)
     state, history = descend_resident(eng, tabs, table, smp_dev, cfg.fcc_sample_count, max_rounds,
                                       stop_on_fixed_point)
     return state.friends, history

@@ -75,9 +75,17 @@ class CudaOps:
     def __init__(self, device: torch.device):
         self.device = device
         self._ws = {}
+        self._side = None
 
     def _stream(self) -> int:
         return torch.cuda.current_stream(self.device).cuda_stream
+
+    def _side_stream(self) -> int:
+        """The stream the join's big-table classes run on, concurrently with the
+        rest (the library forks to it and joins back within the call)."""
+        if self._side is None:
+            self._side = torch.cuda.Stream(self.device)
+        return self._side.cuda_stream
 
     def _workspace(self, key: str, nbytes: int) -> torch.Tensor:
         buf = self._ws.get(key)
@@ -107,7 +115,7 @@ class CudaOps:
         nbytes = _lib.load().knnd_local_join_workspace_bytes(n, tabs.dplan, k, csr.lo, csr.hi, max_indeg)
         ws = self._workspace("join", nbytes)
         tabs.join(table, k, csr, max_indeg, out_rows, tally, out_kl, out_ucount, bound_in, bound_out, ws, flags,
-                  self._stream(), peers=tuple(peers))
+                  self._stream(), peers=tuple(peers), side_stream=self._side_stream())
 
     def random_kout(self, state: tuple, n: int, k: int, table: torch.Tensor, out_meta: torch.Tensor,
                     bad: torch.Tensor) -> None:
@@ -147,10 +155,23 @@ class PeerTables:
 
     def __init__(self, bufs: list, peers: list, barrier: Callable[[int], None]):
         self.bufs, self.peers, self.barrier = bufs, peers, barrier
+        # bumped whenever a round starts writing table i: a state holding an
+        # older generation of table i has been overwritten (KnnState checks)
+        self.gen = [0, 0]
 
     def pick(self, table: torch.Tensor) -> int:
         """Index of the table the round reading `table` writes."""
         return 1 if table.data_ptr() == self.bufs[0].data_ptr() else 0
+
+    def index_of(self, table: torch.Tensor) -> int | None:
+        """i if `table` is (a view starting at) this rank's copy of table i."""
+        for i, b in enumerate(self.bufs):
+            if table.data_ptr() == b.data_ptr():
+                return i
+        return None
+
+    def begin_write(self, i: int) -> None:
+        self.gen[i] += 1
 
 
 _PEER_CACHE: dict = {}
@@ -160,8 +181,9 @@ def symmetric_peer_tables(eng: "Engine") -> PeerTables:
     """Both tables in torch symmetric memory (CUDA IPC mappings of every rank's
     buffer over NVLink).  The mapping is a collective (a rendezvous of every
     rank), so it is made once per (device, table shape, group) and reused by
-    later descents — each run() returns its table to the host before the next
-    one starts."""
+    later descents: descend_resident hands out its final table as a private
+    copy, and an intermediate state (on_round) raises once a later round has
+    reused its table (PeerTables.gen)."""
     import torch.distributed._symmetric_memory as symm
 
     group = eng.group if eng.group is not None else dist.group.WORLD
@@ -178,6 +200,29 @@ def symmetric_peer_tables(eng: "Engine") -> PeerTables:
     pt = PeerTables(bufs, peers, lambda i: handles[i].barrier(channel=0))
     _PEER_CACHE[key] = pt
     return pt
+
+
+def peer_capable(eng: "Engine") -> bool:
+    """This rank can map every other rank's device memory: torch symmetric
+    memory is importable and CUDA peer access to each rank's device exists
+    (device indices gathered over the group)."""
+    try:
+        import torch.distributed._symmetric_memory  # noqa: F401
+    except Exception:
+        ok = False
+    else:
+        ok = eng.device.type == "cuda"
+    idx = torch.tensor([eng.device.index if eng.device.index is not None else -1], dtype=torch.int64,
+                       device=eng.device)
+    allidx = [torch.empty_like(idx) for _ in range(eng.shard.world)]
+    dist.all_gather(allidx, idx, group=eng.group)
+    if ok:
+        me = eng.device.index
+        for t in allidx:
+            other = int(t.item())
+            if other != me and (other < 0 or not torch.cuda.can_device_access_peer(me, other)):
+                ok = False
+    return ok
 
 
 def exchange_mode(eng: "Engine") -> str:
@@ -229,6 +274,13 @@ class Engine:
         if peer is not None:
             self.peer = peer
         elif self.peer is None and exchange_mode(self) == "peer":
+            # agree on capability before the rendezvous (a collective every rank
+            # must enter), so no rank waits in it for one that will not come
+            can = torch.tensor([int(peer_capable(self))], dtype=torch.int32, device=self.device)
+            dist.all_reduce(can, op=dist.ReduceOp.MIN, group=self.group)
+            if int(can.item()) == 0:
+                print("knnd: a rank cannot map its peers' tables; using the NCCL all-gather", file=sys.stderr)
+                return False
             try:
                 self.peer = symmetric_peer_tables(self)
             except Exception as exc:  # e.g. no P2P / IPC between these devices
@@ -306,6 +358,7 @@ class Engine:
         if self.peer is not None:
             ip = self.peer.pick(table)
             nxt, peers = self.peer.bufs[ip], self.peer.peers[ip]
+            self.peer.begin_write(ip)
         else:
             nxt, peers = self.alloc_table(), ()
         s = self.shard

@@ -140,12 +140,12 @@ class DeviceTables:
 
     # -- the kernel calls (one per ABI entry; the L2 tables provide the same methods)
     def join(self, table, k, csr, max_indeg, out_rows, tally, out_scores, out_ucount, bound_in, bound_out, ws,
-             flags, stream, peers=()):
+             flags, stream, peers=(), side_stream=None):
         _lib.call("knnd_local_join_peers", self.points.data_ptr(), self.log32.data_ptr(), self.log64.data_ptr(),
                   self.xlogx.data_ptr(), self.n, self.d, self.ld, table.data_ptr(), k, csr.indptr.data_ptr(),
                   csr.indices.data_ptr(), csr.lo, csr.hi, max_indeg, out_rows.data_ptr(), _ptr(out_scores),
                   _ptr(out_ucount), tally.data_ptr(), _ptr(bound_in), _ptr(bound_out), ws.data_ptr(), ws.numel(),
-                  flags, _lib.peer_array(peers), len(peers), stream)
+                  flags, _lib.peer_array(peers), len(peers), stream, side_stream)
 
     def join_flags(self) -> int:
         return _lib.JOIN_NONPOS_LOG if self.max_coord <= 1.0 else 0
@@ -192,12 +192,13 @@ class L2Tables:
         torch.cuda.current_stream(device).synchronize()  # v and center are temporaries
 
     def join(self, table, k, csr, max_indeg, out_rows, tally, out_scores, out_ucount, bound_in, bound_out, ws,
-             flags, stream, peers=()):
+             flags, stream, peers=(), side_stream=None):
         _lib.call("knnd_l2_local_join_peers", self.anchor32.data_ptr(), self.cand32.data_ptr(),
                   self.rows64.data_ptr(), self.sq64.data_ptr(), self.n, self.d, self.ld, self.maxnorm,
                   table.data_ptr(), k, csr.indptr.data_ptr(), csr.indices.data_ptr(), csr.lo, csr.hi, max_indeg,
                   out_rows.data_ptr(), _ptr(out_scores), _ptr(out_ucount), tally.data_ptr(), _ptr(bound_in),
-                  _ptr(bound_out), ws.data_ptr(), ws.numel(), _lib.peer_array(peers), len(peers), stream)
+                  _ptr(bound_out), ws.data_ptr(), ws.numel(), _lib.peer_array(peers), len(peers), stream,
+                  side_stream)
 
     def join_flags(self) -> int:
         return 0
@@ -214,6 +215,47 @@ class L2Tables:
         _lib.call("knnd_l2_exact_knn", self.anchor32.data_ptr(), self.cand32.data_ptr(), self.rows64.data_ptr(),
                   self.sq64.data_ptr(), self.n, self.d, self.ld, self.maxnorm, q.data_ptr(), q.numel(), k, cap,
                   ids.data_ptr(), _ptr(scores), count.data_ptr(), ws.data_ptr(), ws.numel(), stream)
+
+
+def _index_ids(x, ids, n: int) -> tuple[int, np.ndarray]:
+    """The anchor and candidate ids of batch_scores as numpy indexing reads
+    them in the reference (``self._xlogx[x]``, ``self._log[ids]``): negative
+    values wrap, anything outside [-n, n) raises IndexError, boolean masks
+    select.  Returns (x, int32 ids) ready for the device (n < 2^31)."""
+    xi = int(np.asarray(x).item()) if not isinstance(x, (int, np.integer)) else int(x)
+    if not -n <= xi < n:
+        raise IndexError(f"index {xi} is out of bounds for axis 0 with size {n}")
+    xi %= n
+    if ids is None:
+        return xi, np.arange(n, dtype=np.int32)
+    arr = np.asarray(ids)
+    if arr.dtype == np.bool_:
+        if arr.shape != (n,):
+            raise IndexError(f"boolean index did not match indexed array along axis 0; size of axis is {n} "
+                             f"but size of corresponding boolean axis is {arr.shape[0] if arr.ndim else 1}")
+        return xi, np.nonzero(arr)[0].astype(np.int32)
+    if arr.size and not np.issubdtype(arr.dtype, np.integer):
+        raise IndexError("arrays used as indices must be of integer (or boolean) type")
+    flat = arr.astype(np.int64, copy=False).ravel()
+    if flat.size:
+        lo, hi = int(flat.min()), int(flat.max())
+        if lo < -n or hi >= n:
+            bad = lo if lo < -n else hi
+            raise IndexError(f"index {bad} is out of bounds for axis 0 with size {n}")
+        if lo < 0:
+            flat = np.where(flat < 0, flat + n, flat)
+    return xi, flat.astype(np.int32)
+
+
+def _batch_scores(tab, x, ids) -> np.ndarray:
+    xi, idx = _index_ids(x, ids, tab.n)
+    if idx.size == 0:
+        return np.empty(0, dtype=np.float64)
+    dev_ids = torch.from_numpy(np.ascontiguousarray(idx)).to(tab.device)
+    out = torch.empty(idx.size, dtype=torch.float64, device=tab.device)
+    with torch.cuda.device(tab.device):
+        tab.batch_scores_call(xi, dev_ids, idx.size, out, _stream(tab.device))
+    return out.cpu().numpy()
 
 
 class KlRankingSystem(ScoredRankingSystem):
@@ -244,16 +286,9 @@ class KlRankingSystem(ScoredRankingSystem):
         self._tables.clear()
 
     def batch_scores(self, x: ItemId, ids: np.ndarray | None = None, device=None) -> np.ndarray:
-        """Exact fp64 D(x||y) for ids (all items when None), computed on the GPU."""
-        tab = self.device_tables(device)
-        idx = np.arange(tab.n, dtype=np.int32) if ids is None else np.asarray(ids, dtype=np.int64).astype(np.int32)
-        if idx.size == 0:
-            return np.empty(0, dtype=np.float64)
-        dev_ids = torch.from_numpy(np.ascontiguousarray(idx)).to(tab.device)
-        out = torch.empty(idx.size, dtype=torch.float64, device=tab.device)
-        with torch.cuda.device(tab.device):
-            tab.batch_scores_call(x, dev_ids, idx.size, out, _stream(tab.device))
-        return out.cpu().numpy()
+        """Exact fp64 D(x||y) for ids (all items when None), computed on the GPU;
+        ids index like numpy (negative wrap, out of range raises IndexError)."""
+        return _batch_scores(self.device_tables(device), x, ids)
 
 
 class EuclideanRankingSystem(ScoredRankingSystem):
@@ -283,15 +318,7 @@ class EuclideanRankingSystem(ScoredRankingSystem):
         self._tables.clear()
 
     def batch_scores(self, x: ItemId, ids: np.ndarray | None = None, device=None) -> np.ndarray:
-        tab = self.device_tables(device)
-        idx = np.arange(tab.n, dtype=np.int32) if ids is None else np.asarray(ids, dtype=np.int64).astype(np.int32)
-        if idx.size == 0:
-            return np.empty(0, dtype=np.float64)
-        dev_ids = torch.from_numpy(np.ascontiguousarray(idx)).to(tab.device)
-        out = torch.empty(idx.size, dtype=torch.float64, device=tab.device)
-        with torch.cuda.device(tab.device):
-            tab.batch_scores_call(x, dev_ids, idx.size, out, _stream(tab.device))
-        return out.cpu().numpy()
+        return _batch_scores(self.device_tables(device), x, ids)
 
 
 def euclidean_ranking(vectors) -> EuclideanRankingSystem:

@@ -104,6 +104,54 @@ def test_fcc_schedule_is_round_indexed():
         assert np.array_equal(sched[r - 1], b2.fcc_samples(5000, 10, 1000, b2.derive_rng(4, 3, r)))
 
 
+def test_fcc_schedule_draws_chunks_on_demand():
+    """FccSchedule (what run() uses) gives every round the sample of the
+    up-front schedule, drawing only the chunks the rounds reach."""
+    import torch
+
+    from paper_2202_00517_b200.descent import FccSchedule, draw_fcc_schedule
+
+    cfg = b2.DescentConfig(k=10, seed=4)
+    full = draw_fcc_schedule(5000, 10, cfg, 11)
+    sched = FccSchedule(5000, 10, cfg, 11, torch.device("cpu"))
+    assert len(sched) == 11 and not sched._chunks
+    for r in (1, 2, 5, 9, 11):
+        assert np.array_equal(sched[r - 1].numpy(), full[r - 1])
+    assert list(sched._chunks) == [2]  # only the last chunk touched is kept
+    with pytest.raises(IndexError):
+        sched[11]
+
+
+def test_k_above_device_limit_is_a_config_error():
+    b2.DescentConfig(k=64)
+    with pytest.raises(b2.ConfigError, match="<= 64"):
+        b2.DescentConfig(k=65)
+
+
+def test_batch_score_ids_index_like_numpy():
+    """ids of batch_scores follow numpy indexing (the reference's self._log[ids]):
+    negative ids wrap, out-of-range ids raise IndexError, masks select."""
+    from paper_2202_00517_b200.similarity import _index_ids
+
+    n = 10
+    ref = np.arange(n)
+    for ids in ([0, 9, -1, -10], np.array([3, -3], dtype=np.int16), [], np.arange(n) % 2 == 0):
+        x, got = _index_ids(-2, ids, n)
+        assert x == 8 and got.dtype == np.int32
+        assert np.array_equal(got, ref[np.asarray(ids, dtype=None if len(ids) else np.int64)])
+    assert np.array_equal(_index_ids(3, None, n)[1], ref)
+    for bad in ([10], [-11], [0, 2**40]):
+        with pytest.raises(IndexError):
+            _index_ids(0, bad, n)
+        with pytest.raises(IndexError):
+            ref[np.asarray(bad)]
+    for badx in (10, -11):
+        with pytest.raises(IndexError):
+            _index_ids(badx, [0], n)
+    with pytest.raises(IndexError):
+        _index_ids(0, np.array([0.5]), n)
+
+
 @pytest.mark.parametrize("n,world", [(10, 1), (10, 3), (1_000_000, 8), (7, 8), (100_001, 2)])
 def test_shards_cover_rows_once(n, world):
     shards = [Shard(r, world, n) for r in range(world)]

@@ -56,7 +56,7 @@ def _worker(rank, world, port, meta, out, shared=None):
         smp = torch.from_numpy(draw_fcc_schedule(n, k, cfg, rounds))
         state, hist = descend_resident(eng, tab, table, smp, cfg.fcc_sample_count, rounds)
         if shared is not None:
-            assert state._table.data_ptr() in (shared[rank][0].data_ptr(), shared[rank][1].data_ptr())
+            assert state._table.data_ptr() not in (shared[rank][0].data_ptr(), shared[rank][1].data_ptr())  # a private copy
         out[rank] = {"sha": sha_i32(state.friends),
                      "hist": [(h.comparisons, h.changed_friend_sets, h.fcc) for h in hist]}
     finally:
@@ -114,6 +114,7 @@ def _consensus_worker(rank, world, port, out):
             return E.PeerTables([eng.alloc_table(), eng.alloc_table()], [[], []], lambda i: None)
 
         E.exchange_mode = lambda eng: "peer"
+        E.peer_capable = lambda eng: True
         E.symmetric_peer_tables = mapped
         eng = E.Engine(100, 4, torch.device("cpu"), ops=object())
         out[rank] = (eng.enable_peer_exchange(), eng.peer is None)
