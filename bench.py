@@ -22,7 +22,10 @@ are input generation here and are timed in `e2e`.
              bounded sample of the same workload: the full round-1 local join
              (all anchors of the round-1 input table)
 
-`--impl reference` times that CPU implementation alone (rank 0 only).
+`--impl reference` (rank 0 only) times the same step on the host: a full
+descent with the C restatement on every host thread (row sort, then rounds
+to FCC termination), plus the Python reference package (baseline/_ref) on C1
+and on a C3 round-1 sample for context.
 """
 
 from __future__ import annotations
@@ -39,6 +42,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 METRIC = "KL comparisons/sec + time-to-termination, n=1M d=20 K=20, at 1/2/4/8 B200"
 UNIT = "comparisons/s"
@@ -67,6 +71,8 @@ def parse():
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-recall", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-python-reference", action="store_true",
+                    help="reference arm: skip the Python reference context timings")
     return ap.parse_args()
 
 
@@ -160,31 +166,118 @@ def cpu_threads():
     return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
 
 
+REF_MAX_STEPS = 5  # full CPU descents timed by the reference arm (each ~15-25 s on the box's cores)
+
+
+def cpu_descent(tab, draws, n, k, seed, max_rounds):
+    """One full descent with the C restatement, the GPU arm's step on the host:
+    initial row sort (descent.py:163-174), then rounds of transpose + local
+    join + FCC (descent.py:282-314, 317-338) until the clustering rate stalls
+    (descent.py:360-361).  Returns (comparisons, seconds, rounds, final table)."""
+    from oracle import native
+
+    t0 = time.perf_counter()
+    init = native.sort_rows(tab, draws)
+    final, hist = native.descend(tab, init, seed, 1000, max_rounds)
+    return sum(h["comparisons"] for h in hist), time.perf_counter() - t0, len(hist), final
+
+
+def python_reference_context(seed):
+    """The reference package itself (baseline/_ref, installed from /root/reference),
+    for context beside the C restatement: C1 to termination through its own
+    run_experiment (bench.py:136-184, workers=1, its benchmarking default), and
+    its round-1 join on the first 10,000 anchors of C3 (_propose_block,
+    descent.py:262-279, over the reference's KnnState of the C3 initial table).
+    None when baseline/_ref is absent."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "rankdescent")):
+        return None
+    sys.path.insert(0, ref)
+    try:
+        import rankdescent as rd
+        from rankdescent import descent as rdd
+    finally:
+        sys.path.remove(ref)
+    from oracle import native, port
+
+    out = {"package": "rankdescent (baseline/_ref, pip-installed from /root/reference)", "threads": 1}
+    t0 = time.perf_counter()
+    rep = rd.run_experiment(rd.ExperimentSpec(n=10_000, d=5, k=10, seed=seed, recall_mode="off", workers=1))
+    wall = time.perf_counter() - t0
+    rounds = rep.rounds if hasattr(rep, "rounds") else None
+    comps = sum(r.comparisons for r in rounds) if rounds else None
+    tot = float(rep.total_duration_sec)  # its own timed region: init + rounds (bench.py:155-157)
+    out["c1_run_experiment"] = {"total_duration_s": tot, "wall_s": wall, "rounds": len(rounds) if rounds else None,
+                                "comparisons": comps, "comparisons_per_s": comps / tot if comps else None}
+    n, d, k = CONFIGS["c3"]
+    pts = port.experiment_points(n, d, seed)
+    init = native.sort_rows(native.Tables(pts), port.random_kout_draws(n, k, port.substream(seed, port.TAG_INIT)))
+    rs = rd.KlRankingSystem(pts, validate=False)
+    state = rd.KnnState(init.astype(np.int64))
+    m = 10_000
+    buf = np.empty((n, k), dtype=np.int64)
+    t0 = time.perf_counter()
+    c, _ = rdd._propose_block(0, m, state, rs, buf)
+    dt = time.perf_counter() - t0
+    out["c3_round1_join_sample"] = {"anchors": m, "comparisons": int(c), "wall_s": dt, "comparisons_per_s": c / dt}
+    return out
+
+
 def reference_arm(args):
+    """The reference's algorithm on the box's host cores (rank 0 only): the C
+    restatement (oracle/knnd_oracle.c, every host thread) running the same
+    step as the B200 arm — a full descent from the seeded initial draws — so
+    `value` and the time to termination compare like for like.  The Python
+    reference package itself is timed beside it for context."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    from oracle import native, port
+
     n, d, k = CONFIGS[args.config]
-    tab, init, csr, sample = cpu_sample_setup(n, d, k, args.seed)
-    for _ in range(args.warmup):
-        cpu_sample_run(tab, init, csr, sample)
+    pts = port.experiment_points(n, d, args.seed)
+    tab = native.Tables(pts)
+    draws = port.random_kout_draws(n, k, port.substream(args.seed, port.TAG_INIT))
+    max_rounds = port.round_cap(n, k)
+    # warm-up: a round-1 join over a tenth of the anchors (threads, page faults)
+    init = native.sort_rows(tab, draws)
+    csr = native.transpose(init)
+    for _ in range(max(1, min(args.warmup, 1))):
+        native.local_join(tab, init, np.arange(0, n, 10, dtype=np.int64), csr=csr)
+    del init, csr
+    steps = max(1, min(args.steps, REF_MAX_STEPS))
     comps = secs = 0.0
-    for _ in range(args.steps):
-        c, s = cpu_sample_run(tab, init, csr, sample)
+    rounds = []
+    final = None
+    for _ in range(steps):
+        c, sec, r, final = cpu_descent(tab, draws, n, k, args.seed, max_rounds)
         comps += c
-        secs += s
+        secs += sec
+        rounds.append(r)
     v = comps / secs
     cores = cpu_threads()
-    sample_desc = (f"round-1 local join (descent.py:230-242) of {sample.size} anchors of "
-                   f"{args.config.upper()} via the C oracle, {cores} OpenMP threads")
+    from parity import sha_i32  # tests/parity.py: the repo's table sha convention
+
+    sample_desc = (f"full {args.config.upper()} descent per step (initial row sort, then transpose + local join "
+                   f"+ FCC per round to FCC termination) via the C restatement, {cores} OpenMP threads; "
+                   f"{steps} of {args.steps} requested steps timed (each {secs / steps:.2f} s)")
+    py = None
+    if not args.no_python_reference:
+        try:
+            py = python_reference_context(args.seed)
+        except Exception as exc:  # context only: never fail the arm on it
+            py = {"error": f"{type(exc).__name__}: {exc}"}
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_desc(args.config, n, d, k) + " [CPU: bounded anchor sample]",
-                   "n": n, "d": d, "k": k, "seed": args.seed, "parallelism": "host threads"},
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
+        "steps_requested": args.steps, "warmup": args.warmup, "ms_per_step": secs / steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_desc(args.config, n, d, k), "n": n, "d": d, "k": k, "seed": args.seed,
+                   "rounds_per_step": rounds, "comparisons_per_step": comps / steps,
+                   "time_to_termination_ms": secs / steps * 1e3, "final_table_sha256": sha_i32(final),
+                   "parallelism": "host threads"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample_desc},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "python_reference": py,
     }
     print(json.dumps(line), flush=True)
 
@@ -329,9 +422,17 @@ def b200_arm(args):
             continue  # the first calls warm torch's pinned host-memory cache
         e2e_s += dt
         e2e_comps += sum(h.comparisons for h in hist)
-        s = eng.shard
-        h2d = n * d * 8 + (s.hi - s.lo) * k * 4 + max_rounds * 3 * cfg.fcc_sample_count * 4
-        d2h = n * k * 4 + 64 * len(hist)
+        # what run() copies: the fp64 points up; the FCC samples of the rounds
+        # run, in chunks of FccSchedule.CHUNK rounds (3 x S int32 each) — the
+        # initial table is drawn on the device (only rows with a repeated id,
+        # ~none, are redrawn on the host and uploaded); down: the final table
+        # widened to int64 on the device, the 64-byte round stats per round and
+        # the 16-byte draw metadata
+        from paper_2202_00517_b200.descent import FccSchedule
+
+        chunks = -(-len(hist) // FccSchedule.CHUNK)
+        h2d = n * d * 8 + chunks * FccSchedule.CHUNK * 3 * cfg.fcc_sample_count * 4
+        d2h = n * k * 8 + 64 * len(hist) + 16
     tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)

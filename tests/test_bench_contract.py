@@ -23,7 +23,7 @@ def _bench(*argv, env=None):
 
 
 def test_reference_arm_line():
-    p = _bench("--impl", "reference", "--config", "c1", "--steps", "2", "--warmup", "1")
+    p = _bench("--impl", "reference", "--config", "c1", "--steps", "2", "--warmup", "1", "--no-python-reference")
     assert p.returncode == 0, p.stderr
     lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1
@@ -34,6 +34,12 @@ def test_reference_arm_line():
     cb = d["cpu_baseline"]
     assert cb["value"] == d["value"] and cb["kind"] in ("port", "reference") and cb["cores"] >= 1 and cb["sample"]
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    # a step is the full descent (like the B200 arm's): the reference's own C1 trajectory
+    with open(os.path.join(ROOT, "tests", "golden", "trajectories.json")) as fh:
+        ref = json.load(fh)["c1"]
+    assert d["config"]["rounds_per_step"] == [ref["rounds_used"]] * 2
+    assert d["config"]["comparisons_per_step"] == sum(r["comparisons"] for r in ref["rounds"])
+    assert d["config"]["final_table_sha256"] == ref["rounds"][-1]["sha"]
 
 
 def test_reference_arm_other_ranks_are_silent():
