@@ -201,9 +201,12 @@ int knnd_random_kout(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint
  * number of candidates kept; a value > cap means row a was NOT written and
  * must be recomputed with cap >= out_count[a].  out_scores (nullable) gets
  * the fp64 scores.  flags: KNND_JOIN_NONPOS_LOG as for the local join.
- * Workspace: knnd_exact_knn_workspace_bytes(nq, cap).  K in 1..64.
+ * The screen runs on the tensor cores (tcgen05.mma kind::tf32, band widened to
+ * the tf32 error); ld32 <= 96 here.
+ * Workspace: knnd_exact_knn_workspace_bytes(n, ld32, nq, cap) (the candidate
+ * lists and a re-tiled copy of the candidate table).  K in 1..64.
  */
-size_t knnd_exact_knn_workspace_bytes(int64_t nq, int32_t cap);
+size_t knnd_exact_knn_workspace_bytes(int64_t n, int32_t ld32, int64_t nq, int32_t cap);
 int knnd_exact_knn(const double *points, const float *log32, const double *log64,
                    const double *xlogx, int64_t n, int32_t d, int32_t ld32,
                    const int32_t *queries, int64_t nq, int32_t k, int32_t cap,

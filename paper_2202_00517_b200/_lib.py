@@ -41,7 +41,7 @@ _SIGS = {
                                _P, _P, _P, _P, _SZ, C.c_uint32, _P, _I32, _P, _P], C.c_int),
     "knnd_fcc": ([_P, _I64, _I32, _P, _P, _P, _I32, _P, _P], C.c_int),
     "knnd_sort_rows": ([_P, _P, _P, _I64, _I32, _I32, _I64, _I64, _P, _P, _P, _P], C.c_int),
-    "knnd_exact_knn_workspace_bytes": ([_I64, _I32], _SZ),
+    "knnd_exact_knn_workspace_bytes": ([_I64, _I32, _I64, _I32], _SZ),
     "knnd_exact_knn": ([_P, _P, _P, _P, _I64, _I32, _I32, _P, _I64, _I32, _I32, _P, _P, _P, _P, _SZ, C.c_uint32, _P],
                        C.c_int),
     "knnd_l2_prepare": ([_P, _P, _I64, _I32, _I32, _P, _P, _P, _P, _P], C.c_int),

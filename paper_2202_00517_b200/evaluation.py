@@ -23,8 +23,14 @@ from .core import ConfigError, Dataset, ItemId
 from .descent import STREAM_RECALL, derive_rng
 from .similarity import device_tables_for
 
-_BATCH = 1 << 16  # queries per device call (bounds the candidate lists)
-_CAP = 256  # initial candidate-list capacity per query (rows that overflow are rerun)
+_QCTA = 256  # queries per CTA of the tensor-core screen (exact.cu TC_Q)
+
+
+def _batch(device) -> int:
+    """Queries per device call: whole waves of the screen's CTAs (one per SM),
+    four waves per call (bounds the candidate lists to ~600 MB at cap 1024)."""
+    return torch.cuda.get_device_properties(device).multi_processor_count * _QCTA * 4
+_CAP = 1024  # initial candidate-list capacity per query (rows that overflow are rerun: a whole extra pass)
 
 
 @dataclass
@@ -47,7 +53,7 @@ class ExactKnnGraph:
 
 def _exact_call(tabs, q: torch.Tensor, k: int, cap: int, ids: torch.Tensor, scores: torch.Tensor | None,
                 count: torch.Tensor) -> None:
-    nbytes = _lib.load().knnd_exact_knn_workspace_bytes(q.numel(), cap)
+    nbytes = _lib.load().knnd_exact_knn_workspace_bytes(tabs.n, tabs.ld, q.numel(), cap)
     ws = torch.empty(nbytes, dtype=torch.uint8, device=tabs.device)
     tabs.exact(q, k, cap, ids, scores, count, ws, torch.cuda.current_stream(tabs.device).cuda_stream)
 
@@ -65,22 +71,27 @@ def exact_rows_device(rs, queries, k: int, device=None, with_scores: bool = Fals
     q_all = torch.from_numpy(qh.astype(np.int32)).to(tabs.device)
     ids = torch.empty((qh.size, k), dtype=torch.int32, device=tabs.device)
     scores = torch.empty((qh.size, k), dtype=torch.float64, device=tabs.device) if with_scores else None
-    for lo in range(0, qh.size, _BATCH):
-        hi = min(lo + _BATCH, qh.size)
+    step = _batch(tabs.device)
+    for lo in range(0, qh.size, step):
+        hi = min(lo + step, qh.size)
         q = q_all[lo:hi]
         count = torch.empty(hi - lo, dtype=torch.int32, device=tabs.device)
         _exact_call(tabs, q, k, _CAP, ids[lo:hi], scores[lo:hi] if with_scores else None, count)
-        over = torch.nonzero(count > _CAP).flatten()
-        if over.numel():  # rare: many candidates inside the error band (e.g. duplicate points)
-            cap = int(count[over].max().item())
-            q2 = q[over].contiguous()
+        cap, sel, cnt = _CAP, torch.arange(hi - lo, device=tabs.device), count
+        over = torch.nonzero(cnt > cap).flatten()
+        while over.numel():  # rare: many candidates inside the error band (e.g. duplicate points)
+            cap = max(int(cnt[over].max().item()), 2 * cap)
+            sel = sel[over]
+            q2 = q[sel].contiguous()
             ids2 = torch.empty((q2.numel(), k), dtype=torch.int32, device=tabs.device)
             sc2 = torch.empty((q2.numel(), k), dtype=torch.float64, device=tabs.device) if with_scores else None
-            c2 = torch.empty(q2.numel(), dtype=torch.int32, device=tabs.device)
-            _exact_call(tabs, q2, k, cap, ids2, sc2, c2)
-            ids[lo:hi][over] = ids2
+            cnt = torch.empty(q2.numel(), dtype=torch.int32, device=tabs.device)
+            _exact_call(tabs, q2, k, cap, ids2, sc2, cnt)
+            ok = cnt <= cap  # rows written by this call
+            ids[lo:hi][sel[ok]] = ids2[ok]
             if with_scores:
-                scores[lo:hi][over] = sc2
+                scores[lo:hi][sel[ok]] = sc2[ok]
+            over = torch.nonzero(~ok).flatten()
     return (ids, scores) if with_scores else ids
 
 
