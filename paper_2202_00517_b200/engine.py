@@ -310,9 +310,24 @@ class Engine:
             return
         flat = table.view(-1)
         mine = flat[s.rank * s.chunk * self.k:(s.rank + 1) * s.chunk * self.k]
-        if dist.get_backend(self.group) != "nccl":
-            mine = mine.clone()  # NCCL gathers in place; other backends want a separate input
-        dist.all_gather_into_tensor(flat, mine, group=self.group)
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_gather_into_tensor(flat, mine, group=self.group)  # in place
+        elif flat.is_cuda:  # gloo (tests: several ranks on one device): through host memory
+            host = flat.cpu()
+            dist.all_gather_into_tensor(host, host[s.rank * s.chunk * self.k:(s.rank + 1) * s.chunk * self.k].clone(),
+                                        group=self.group)
+            flat.copy_(host)
+        else:
+            dist.all_gather_into_tensor(flat, mine.clone(), group=self.group)
+
+    def all_reduce(self, t: torch.Tensor) -> None:
+        """Sum over ranks (NCCL; gloo stages CUDA tensors through host memory)."""
+        if dist.get_backend(self.group) != "nccl" and t.is_cuda:
+            host = t.cpu()
+            dist.all_reduce(host, group=self.group)
+            t.copy_(host)
+        else:
+            dist.all_reduce(t, group=self.group)
 
     def upload_rows(self, host_rows: np.ndarray, table: torch.Tensor) -> int:
         """Copy this rank's rows of a host (n, K) table into `table`; returns bytes copied."""
@@ -377,7 +392,7 @@ class Engine:
                 self.peer.barrier(ip)  # every rank's rows are in every copy
             else:
                 self.exchange(nxt)
-            dist.all_reduce(tally, group=self.group)
+            self.all_reduce(tally)
         csr_next = self.ops.csr(nxt, self.n, self.k, s.lo, s.hi, self._stats32[9:10])
         if samples is not None:
             self.ops.fcc(nxt, self.n, self.k, samples, self._stats32[8:9])
