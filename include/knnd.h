@@ -46,6 +46,12 @@ int knnd_abi_version(void);
 const char *knnd_last_error(void);
 /* Number of kernels this library has launched in this process (all threads). */
 unsigned long long knnd_launch_count(void);
+/* Checked build only (libknnd_checked.so, compiled with -DKNND_CHECKED): the
+ * number of device-side bounds checks that failed since the last call, and
+ * the first failure's location (file id * 100000 + line); both are cleared.
+ * The product build returns KNND_EUNSUPPORTED (its checks are compiled out).
+ * Synchronises with the device. */
+int knnd_check_failures(unsigned long long *count, unsigned long long *first);
 
 /*
  * KlRankingSystem.__init__ precompute (similarity.py:87-95):

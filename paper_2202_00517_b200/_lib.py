@@ -8,7 +8,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-from .build import LIB_PATH
+from .build import CHECKED_LIB_PATH, LIB_PATH
 
 _lib = None
 
@@ -30,6 +30,7 @@ _SIGS = {
     "knnd_abi_version": ([], C.c_int),
     "knnd_last_error": ([], C.c_char_p),
     "knnd_launch_count": ([], C.c_ulonglong),
+    "knnd_check_failures": ([_P, _P], C.c_int),
     "knnd_kl_prepare": ([_P, _I64, _I32, _I32, _P, _P, _P, _P], C.c_int),
     "knnd_batch_scores": ([_P, _P, _P, _I64, _I32, _I64, _P, _I64, _P, _P], C.c_int),
     "knnd_csr_workspace_bytes": ([_I64, _I32, _I64, _I64], _SZ),
@@ -76,7 +77,9 @@ def load(path: str | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    path = path or LIB_PATH
+    # KNND_LIBRARY=checked selects the bounds-checked build (tests/test_checked.py)
+    env = os.environ.get("KNND_LIBRARY")
+    path = path or (CHECKED_LIB_PATH if env == "checked" else env) or LIB_PATH
     if not os.path.exists(path):
         raise ImportError(
             f"libknnd.so not found at {path}; build it with `python -m paper_2202_00517_b200.build` "

@@ -18,6 +18,9 @@ ROOT = os.path.dirname(PKG_DIR)
 CSRC = os.path.join(PKG_DIR, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB_PATH = os.path.join(PKG_DIR, "libknnd.so")
+# the checked build (-DKNND_CHECKED: device-side bounds checks, knnd_check_failures),
+# used by tests/test_checked.py in place of compute-sanitizer; never by the product
+CHECKED_LIB_PATH = os.path.join(PKG_DIR, "libknnd_checked.so")
 OBJ_DIR = os.path.join(PKG_DIR, "_obj")
 
 SOURCES = ["abi.cu", "prep.cu", "csr.cu", "join.cu", "rng.cu", "exact.cu"]
@@ -46,38 +49,50 @@ def _newest_input() -> float:
     return max(os.path.getmtime(p) for p in paths)
 
 
-def needs_build() -> bool:
-    return not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < _newest_input()
+def needs_build(path: str = LIB_PATH) -> bool:
+    return not os.path.exists(path) or os.path.getmtime(path) < _newest_input()
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, checked: bool = True) -> str:
+    """Build libknnd.so (and, unless checked=False, libknnd_checked.so) in-tree."""
+    targets = [(LIB_PATH, OBJ_DIR, ())]
+    if checked:
+        targets.append((CHECKED_LIB_PATH, OBJ_DIR + "_checked", ("-DKNND_CHECKED",)))
+    targets = [t for t in targets if force or needs_build(t[0])]
+    if not targets:
         return LIB_PATH
     nvcc = nvcc_path()
-    os.makedirs(OBJ_DIR, exist_ok=True)
+    for _, obj_dir, _ in targets:
+        os.makedirs(obj_dir, exist_ok=True)
 
-    def compile_one(src: str) -> tuple[str, str]:
-        obj = os.path.join(OBJ_DIR, src.replace(".cu", ".o"))
-        cmd = [nvcc, *NVCC_FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+    def compile_one(job) -> tuple[str, str]:
+        src, obj_dir, extra = job
+        obj = os.path.join(obj_dir, src.replace(".cu", ".o"))
+        cmd = [nvcc, *NVCC_FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {src}:\n{res.stdout}\n{res.stderr}")
+            raise RuntimeError(f"nvcc failed for {src} {' '.join(extra)}:\n{res.stdout}\n{res.stderr}")
         return obj, res.stderr
 
-    with ThreadPoolExecutor(max_workers=len(SOURCES)) as pool:
-        results = list(pool.map(compile_one, SOURCES))
+    jobs = [(src, obj_dir, extra) for _, obj_dir, extra in targets for src in SOURCES]
+    # the largest translation units first (join.cu dominates the build)
+    jobs.sort(key=lambda j: -os.path.getsize(os.path.join(CSRC, j[0])))
+    with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as pool:
+        results = dict(zip(jobs, pool.map(compile_one, jobs)))
+    for lib_path, obj_dir, extra in targets:
+        objs = [results[(src, obj_dir, extra)][0] for src in SOURCES]
+        tmp = lib_path + ".tmp"
+        cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
+        os.replace(tmp, lib_path)
+        with open(os.path.join(obj_dir, "ptxas.log"), "w") as fh:
+            for src in SOURCES:
+                fh.write(results[(src, obj_dir, extra)][1])
     if verbose:
-        for _, log in results:
+        for _, log in results.values():
             sys.stderr.write(log)
-    tmp = LIB_PATH + ".tmp"
-    cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *[o for o, _ in results]]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
-    os.replace(tmp, LIB_PATH)
-    with open(os.path.join(OBJ_DIR, "ptxas.log"), "w") as fh:
-        for _, log in results:
-            fh.write(log)
     return LIB_PATH
 
 

@@ -49,6 +49,47 @@ int num_sms();
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// ---------------------------------------------------------------------------
+// Checked build (-DKNND_CHECKED -> libknnd_checked.so; the stand-in for
+// compute-sanitizer, which this GPU pool keeps closed): device-side bounds
+// checks on the hand-computed indices — shared-memory slab layouts, hash
+// table / list / staging capacities, workspace offsets, id ranges.  A failed
+// check counts itself and records its source line (the first one wins) in a
+// per-file device word; knnd_check_failures() reads and clears them all.  The
+// product build compiles every check away.
+#ifdef KNND_CHECKED
+static __device__ unsigned long long g_check[2];  // [0] failures, [1] first failing line
+#define KNND_DCHECK(cond)                                                                 \
+  do {                                                                                    \
+    if (!(cond)) {                                                                        \
+      if (atomicAdd(&::knnd::g_check[0], 1ull) == 0ull) ::knnd::g_check[1] = __LINE__;    \
+    }                                                                                     \
+  } while (0)
+// one reader per source file (file id * 100000 + line identifies a failure)
+#define KNND_CHECK_READER(NAME, FILE_ID)                                                   \
+  namespace knnd {                                                                        \
+  int check_read_##NAME(unsigned long long *count, unsigned long long *first) {          \
+    unsigned long long h[2] = {0, 0}, z[2] = {0, 0};                                      \
+    if (cudaMemcpyFromSymbol(h, g_check, sizeof(h)) != cudaSuccess) return KNND_ECUDA;    \
+    if (cudaMemcpyToSymbol(g_check, z, sizeof(z)) != cudaSuccess) return KNND_ECUDA;      \
+    if (h[0] && !*first) *first = (unsigned long long)(FILE_ID) * 100000ull + h[1];      \
+    *count += h[0];                                                                       \
+    return KNND_OK;                                                                       \
+  }                                                                                       \
+  }
+int check_read_abi(unsigned long long *, unsigned long long *);
+int check_read_join(unsigned long long *, unsigned long long *);
+int check_read_exact(unsigned long long *, unsigned long long *);
+int check_read_csr(unsigned long long *, unsigned long long *);
+int check_read_prep(unsigned long long *, unsigned long long *);
+int check_read_rng(unsigned long long *, unsigned long long *);
+#else
+#define KNND_DCHECK(cond) \
+  do {                    \
+  } while (0)
+#define KNND_CHECK_READER(NAME, FILE_ID)
+#endif
+
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 // ---------------------------------------------------------------------------
@@ -180,6 +221,12 @@ struct WarpTopK {
     }
   }
 };
+
+__device__ __forceinline__ unsigned dyn_smem_bytes() {
+  unsigned v;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(v));
+  return v;
+}
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;

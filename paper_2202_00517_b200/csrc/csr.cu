@@ -152,6 +152,7 @@ __global__ void csr_fill_kernel(const int32_t *__restrict__ F, int64_t n, int K,
       int64_t t = (int64_t)__ldg(row + j) - lo;
       if ((uint64_t)t < (uint64_t)m) {
         int pos = atomicAdd(cursor + t, 1);
+        KNND_DCHECK(pos >= 0 && (int64_t)pos < n * K);
         indices[pos] = (int32_t)s;
       }
     }
@@ -218,3 +219,5 @@ int knnd_csr_build(const int32_t *friends, int64_t n, int32_t k, int64_t row_lo,
 }
 
 }  // extern "C"
+
+KNND_CHECK_READER(csr, 3)

@@ -209,6 +209,7 @@ __global__ void tc_image_kernel(const float *__restrict__ c, int64_t n, int ld, 
     if (y < n && k0 < ld) v = *reinterpret_cast<const float4 *>(c + y * ld + k0);  // ld % 4 == 0
     unsigned char *dst = img + (tile * KT + kt) * (int64_t)TC_SUB + (r >> 3) * 1024 + (r & 7) * 128 +
                          ((ch ^ (r & 7)) * 16);
+    KNND_DCHECK(dst + 16 <= img + ((n + TC_BN - 1) / TC_BN) * KT * (int64_t)TC_SUB);
     *reinterpret_cast<float4 *>(dst) = v;
   }
 }
@@ -261,6 +262,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) exact_tc_kernel(TcParams p) {
   float anorm = 0.f;
   if (is_epi) {
     if (qa < p.nq) qid = p.queries[qa];
+    KNND_DCHECK(qid < p.n);
+#ifdef KNND_CHECKED
+    {
+      unsigned dyn;
+      asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+      KNND_DCHECK((size_t)(sm - sm_raw) + L.total <= dyn);
+    }
+#endif
     unsigned char *arow = sm + L.a + (uint32_t)half * KT * TC_M * 128 + (uint32_t)(r >> 3) * 1024 + (uint32_t)(r & 7) * 128;
     for (int kt = 0; kt < KT; ++kt) {
 #pragma unroll 1
@@ -691,3 +700,5 @@ int knnd_l2_exact_knn(const float *anchor32, const float *cand32, const double *
 }
 
 }  // extern "C"
+
+KNND_CHECK_READER(exact, 2)

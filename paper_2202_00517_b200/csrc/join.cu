@@ -54,6 +54,7 @@ struct JoinParams {
   int32_t *__restrict__ out_ucount;
   unsigned long long *tally;
   int64_t lo;
+  int64_t n, m;  // items, own rows (checked build: id and row ranges)
   int d, ld, K;
   float band;
   int nonpos;  // every log coordinate <= 0: sum |x log y| == -sum x log y exactly
@@ -101,6 +102,7 @@ __device__ __forceinline__ bool hash_insert_cas(int32_t *table, int y, unsigned 
     if ((v.x == y) | (v.y == y) | (v.z == y) | (v.w == y)) return false;
     if (v.w == EMPTY) {
       const int occ = 4 + (v.x >> 31) + (v.y >> 31) + (v.z >> 31) + (v.w >> 31);
+      KNND_DCHECK(b * 4 + occ <= mask && occ >= 0 && occ < 4);
       const int prev = atomicCAS(table + b * 4 + occ, EMPTY, y);
       if (prev == EMPTY) return true;
       if (prev == y) return false;
@@ -134,6 +136,7 @@ __device__ __forceinline__ void hash_insert4(int32_t *table, const int (&id)[UNR
     const bool found = (v[u].x == y) | (v[u].y == y) | (v[u].z == y) | (v[u].w == y);
     const bool can = valid[u] && !found && v[u].w == EMPTY;
     const int occ = 4 + (v[u].x >> 31) + (v[u].y >> 31) + (v[u].z >> 31) + (v[u].w >> 31);
+    KNND_DCHECK(!can || (b[u] * 4 + occ <= mask && occ >= 0 && occ < 4));
     prev[u] = can ? atomicCAS(table + b[u] * 4 + occ, EMPTY, y) : EMPTY;  // EMPTY: no CAS made
     nw[u] = can && prev[u] == EMPTY;
     retry[u] = valid[u] && !found && !nw[u] && prev[u] != y;
@@ -449,6 +452,7 @@ __device__ __forceinline__ void collect_r(const float *scores, const int32_t *li
       b0 = __shfl_sync(FULL, b0, leader);
       if (take) {
         const int r = b0 + __popc(m & lanemask_lt());
+        KNND_DCHECK(r < U);  // R (table + H/2) holds up to H/2 >= U ids
         R[r] = list[k];
         if (r < 32) rval[r] = v;
       }
@@ -647,7 +651,9 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
       while (la < logH && (1 << la) < 2 * total) ++la;
       Ha = 1 << la;
       sha = 32u - (unsigned)la;
+      KNND_DCHECK((int64_t)SW + Ha + Ha / 2 <= slab_ints && 2 * total <= Ha);
     }
+    KNND_DCHECK(nS <= SW && xr >= 0 && xr < p.m && x >= 0 && x < p.n);
     // (this anchor's inputs are in buffer pb: the end of the previous anchor
     // waited for them before its barrier; hdr[8..12] is rewritten only after
     // the phase-0 barrier below)
@@ -722,8 +728,10 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
           int b0 = 0;
           if (lane == 0) b0 = atomicAdd(&hdr[0], tot);
           b0 = __shfl_sync(FULL, b0, 0);
+          KNND_DCHECK(b0 + tot <= (Ha >> 1));
 #pragma unroll
           for (int u = 0; u < UNR1; ++u) {
+            KNND_DCHECK(!nw[u] || (id[u] >= 0 && id[u] < p.n));
             if (nw[u]) list[b0 + __popc(m[u] & lanemask_lt())] = id[u];
             b0 += __popc(m[u]);
           }
@@ -764,8 +772,10 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
           int b0 = 0;
           if (lane == 0) b0 = atomicAdd(&hdr[0], tot);
           b0 = __shfl_sync(FULL, b0, 0);
+          KNND_DCHECK(b0 + tot <= (Ha >> 1));
 #pragma unroll
           for (int u = 0; u < UNR1; ++u) {
+            KNND_DCHECK(!nw[u] || (id[u] >= 0 && id[u] < p.n));
             if (nw[u]) list[b0 + __popc(m[u] & lanemask_lt())] = id[u];
             b0 += __popc(m[u]);
           }
@@ -788,6 +798,8 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
       const int per_warp_floats = ((H - u4) / W) & ~3;
       wrows = min(32, per_warp_floats / (2 * ld));
       wstage = reinterpret_cast<float *>(table + u4) + (size_t)warp * per_warp_floats;
+      KNND_DCHECK(U == 0 || (wrows >= 1 && u4 + (size_t)(warp + 1) * per_warp_floats <= (size_t)H &&
+                             2 * wrows * ld <= per_warp_floats));
     }
     float mn = __int_as_float(0x7f800000), mx = -mn, am = 0.f;
     const float slack = p.slack;
@@ -1055,6 +1067,13 @@ __global__ void __launch_bounds__(128, 4)
   unsigned char *base = sm + (size_t)warp * L.total;
   int32_t *table = reinterpret_cast<int32_t *>(base + L.table);
   int32_t *list = reinterpret_cast<int32_t *>(base + L.list);
+#ifdef KNND_CHECKED
+  {
+    unsigned dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    KNND_DCHECK((size_t)(warp + 1) * L.total <= dyn);  // this warp's slab lies inside the launch's smem
+  }
+#endif
   float *scores = reinterpret_cast<float *>(table);            // phase 2-3: [0, U)
   double *stage64 = reinterpret_cast<double *>(table);         // phase 4: whole table
   const int K = p.K, K1 = K + 1;
@@ -1105,6 +1124,7 @@ __global__ void __launch_bounds__(128, 4)
     const float T0 = p.bound_in ? __ldg(p.bound_in + xr) : __int_as_float(0x7fc00000);
     const int nS = K + c;
     const int total = nS * K1;
+    KNND_DCHECK(nS <= SW && xr >= 0 && xr < p.m && x >= 0 && x < p.n);
 
     // ---- phase 0
     {
@@ -1166,8 +1186,10 @@ __global__ void __launch_bounds__(128, 4)
 #pragma unroll
         for (int u = 0; u < UNR1; ++u) {
           const unsigned m = __ballot_sync(FULL, nw[u]);
+          KNND_DCHECK(!nw[u] || (id[u] >= 0 && id[u] < p.n));
           if (nw[u]) list[U + __popc(m & lanemask_lt())] = id[u];
           U += __popc(m);
+          KNND_DCHECK(U <= (H >> 1));
         }
       }
     } else {
@@ -1216,8 +1238,10 @@ __global__ void __launch_bounds__(128, 4)
 #pragma unroll
         for (int u = 0; u < UNR1; ++u) {
           const unsigned m = __ballot_sync(FULL, nw[u]);
+          KNND_DCHECK(!nw[u] || (id[u] >= 0 && id[u] < p.n));
           if (nw[u]) list[U + __popc(m & lanemask_lt())] = id[u];
           U += __popc(m);
+          KNND_DCHECK(U <= (H >> 1));
         }
       }
     }
@@ -1240,6 +1264,7 @@ __global__ void __launch_bounds__(128, 4)
     const int u4 = (U + 3) & ~3;
     float *stage = reinterpret_cast<float *>(table + u4);
     const int rows = min(32, (H - u4) / (ld * 2));
+    KNND_DCHECK(U == 0 || (rows >= 1 && u4 + 2 * rows * ld <= H));
     int id_next = (lane < min(rows, U)) ? list[lane] : 0;
     int id_after = (rows + lane < U && lane < rows) ? list[rows + lane] : 0;
     if (U > 0) {
@@ -1706,6 +1731,8 @@ static int join_run(const char *who, JoinParams &p, int64_t n, int32_t dplan, in
   const int64_t *indptr = p.indptr;
   unsigned long long *tally = p.tally;
   p.lo = row_lo;
+  p.n = n;
+  p.m = m;
   p.K = k;
   // rigorous bound on |fp32 screen - fp64| relative to sum |x*log y| (+ margin)
   p.band = (float)((ld32 + 8) * 0x1p-24);
@@ -1914,3 +1941,5 @@ int knnd_l2_local_join(const float *anchor32, const float *cand32, const double 
 }
 
 }  // extern "C"
+
+KNND_CHECK_READER(join, 1)

@@ -109,8 +109,10 @@ __global__ void sort_rows_kernel(const double *__restrict__ pts, int pstride, co
     const double xl = xlogx[x];
     KeyD key[KPL];
     int idv[KPL];
+    KNND_DCHECK((size_t)(w + 1) * per_warp * 8 <= (size_t)dyn_smem_bytes());
     if (KPL == 1 && staged) {
       const int y = lane < K ? draws[xr * K + lane] : 0;
+      KNND_DCHECK(lane >= K || y >= 0);
       idv[0] = lane < K ? y : -1;
       const int nchunk = K * d64;
       int r = lane / d64, j = lane - (lane / d64) * d64;
@@ -142,6 +144,7 @@ __global__ void sort_rows_kernel(const double *__restrict__ pts, int pstride, co
         idv[q] = -1;
         if (pos < K) {
           int y = draws[xr * K + pos];
+          KNND_DCHECK(y >= 0);
           idv[q] = y;
           key[q] = {exact_score_m(x64, log64 + (int64_t)y * d64, d, xl, metric), pos};
         }
@@ -316,3 +319,5 @@ int knnd_fcc(const int32_t *friends, int64_t n, int32_t k, const int32_t *xs, co
 }
 
 }  // extern "C"
+
+KNND_CHECK_READER(prep, 4)

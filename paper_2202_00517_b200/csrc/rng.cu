@@ -67,6 +67,7 @@ __global__ void __launch_bounds__(RNG_THREADS) rng_pass_kernel(RngArgs a, const 
   const u128 mult = mk(a.mult_hi, a.mult_lo), inc = mk(a.inc_hi, a.inc_lo);
   u128 s = jump(J, mk(a.s_hi, a.s_lo), (unsigned long long)(a.out_base + t * RNG_OUT_PER_THREAD));
   long long pos = WRITE ? offsets[t] : 0;
+  KNND_DCHECK(pos >= 0);
   int cnt = 0;
 #pragma unroll
   for (int o = 0; o < RNG_OUT_PER_THREAD; ++o) {
@@ -157,7 +158,11 @@ __global__ void dup_rows_kernel(const int32_t *__restrict__ T, long long n, int 
       const int32_t v = row[i];
       for (int j = 0; j < i; ++j) dup |= row[j] == v;
     }
-    if (dup) bad[atomicAdd(nbad, 1)] = (int32_t)r;
+    if (dup) {
+      const int at = atomicAdd(nbad, 1);
+      KNND_DCHECK(at >= 0 && at < n);
+      bad[at] = (int32_t)r;
+    }
   }
 }
 
@@ -270,3 +275,5 @@ int knnd_random_kout(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint
 }
 
 }  // extern "C"
+
+KNND_CHECK_READER(rng, 5)

@@ -69,6 +69,34 @@ class Csr:
     hi: int
 
 
+# Workspace guard zones (KNND_GUARD=1; tests/test_checked.py): every workspace
+# gets GUARD bytes of a known pattern on both sides, and check_guards() reports
+# any that a kernel overwrote — the host-side half of the stand-in for
+# compute-sanitizer (the device-side half is the checked build's bounds checks).
+GUARD = 4096
+_GUARD_BYTE = 0x5A
+_guards: list = []
+
+
+def workspace(nbytes: int, device: torch.device) -> torch.Tensor:
+    """A uint8 device workspace of at least nbytes (guarded under KNND_GUARD=1)."""
+    nbytes = max(int(nbytes), 256)
+    if os.environ.get("KNND_GUARD") != "1":
+        return torch.empty(nbytes, dtype=torch.uint8, device=device)
+    raw = torch.full((nbytes + 2 * GUARD,), _GUARD_BYTE, dtype=torch.uint8, device=device)
+    _guards.append(raw)
+    return raw[GUARD:GUARD + nbytes]
+
+
+def check_guards() -> int:
+    """Number of guard bytes overwritten since the workspaces were made (0 = clean)."""
+    bad = 0
+    for raw in _guards:
+        n = raw.numel() - 2 * GUARD
+        bad += int((raw[:GUARD] != _GUARD_BYTE).sum()) + int((raw[GUARD + n:] != _GUARD_BYTE).sum())
+    return bad
+
+
 class CudaOps:
     """The product kernel calls (libknnd.so) on one device's current stream."""
 
@@ -90,7 +118,7 @@ class CudaOps:
     def _workspace(self, key: str, nbytes: int) -> torch.Tensor:
         buf = self._ws.get(key)
         if buf is None or buf.numel() < nbytes:
-            buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+            buf = workspace(nbytes, self.device)
             self._ws[key] = buf
         return buf
 

@@ -21,6 +21,7 @@ import torch
 from . import _lib
 from .core import ConfigError, Dataset, ItemId
 from .descent import STREAM_RECALL, derive_rng
+from .engine import workspace
 from .similarity import device_tables_for
 
 _QCTA = 256  # queries per CTA of the tensor-core screen (exact.cu TC_Q)
@@ -54,7 +55,7 @@ class ExactKnnGraph:
 def _exact_call(tabs, q: torch.Tensor, k: int, cap: int, ids: torch.Tensor, scores: torch.Tensor | None,
                 count: torch.Tensor) -> None:
     nbytes = _lib.load().knnd_exact_knn_workspace_bytes(tabs.n, tabs.ld, q.numel(), cap)
-    ws = torch.empty(nbytes, dtype=torch.uint8, device=tabs.device)
+    ws = workspace(nbytes, tabs.device)
     tabs.exact(q, k, cap, ids, scores, count, ws, torch.cuda.current_stream(tabs.device).cuda_stream)
 
 

@@ -41,6 +41,17 @@ def test_every_declared_symbol_is_exported(lib):
         assert re.search(rf"\bT {name}\b", out), name
 
 
+def test_checked_build_exports_the_same_abi(lib):
+    """libknnd_checked.so (bounds-checked, tests/test_checked.py) exports the same
+    ABI; the product build compiles the checks out and says so."""
+    out = subprocess.run(["nm", "-D", "--defined-only", build.CHECKED_LIB_PATH], capture_output=True, text=True).stdout
+    for name in declared_symbols():
+        assert re.search(rf"\bT {name}\b", out), name
+    cnt, first = C.c_ulonglong(7), C.c_ulonglong(7)
+    assert lib.knnd_check_failures(C.byref(cnt), C.byref(first)) == -4  # KNND_EUNSUPPORTED
+    assert "product build" in _lib.last_error() and (cnt.value, first.value) == (0, 0)
+
+
 def test_library_is_sm100a_code():
     out = subprocess.run(["cuobjdump", "--list-elf", build.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out

@@ -1,5 +1,9 @@
 """A small run of every libknnd kernel, for compute-sanitizer (memcheck /
-racecheck / synccheck; tools/gpu_sanitize.sh, tests/test_sanitize.py).
+racecheck / synccheck; tools/gpu_sanitize.sh, tests/test_sanitize.py) and for
+its stand-in on pools where compute-sanitizer is closed: run with
+KNND_LIBRARY=checked KNND_GUARD=1 (tests/test_checked.py) it loads the
+bounds-checked build and guards every workspace, and fails unless
+knnd_check_failures() and the guard zones both report zero.
 
 Covers: kl_prepare, the device PCG64 draws (knnd_random_kout) + row sort,
 co-friend CSR, the local join in every size class (warp, 2^12/2^13 128-thread
@@ -88,7 +92,34 @@ def main():
     b2.run_round(est, ers, ecfg)
     b2.exact_rows(ers, np.arange(0, 3000, 97), 10)
     torch.cuda.synchronize()
+    report_checks()
     print("SANITIZE_OK", flush=True)
+
+
+def report_checks():
+    """Checked build / guarded workspaces: zero failed bounds checks, zero guard bytes touched."""
+    import ctypes as C
+
+    from paper_2202_00517_b200 import _lib
+    from paper_2202_00517_b200.engine import check_guards
+
+    if os.environ.get("KNND_GUARD") == "1":
+        bad = check_guards()
+        print(f"guard bytes overwritten: {bad}", flush=True)
+        assert bad == 0, f"{bad} workspace guard bytes were overwritten"
+    if os.environ.get("KNND_LIBRARY") == "checked":
+        cnt, first = C.c_ulonglong(0), C.c_ulonglong(0)
+        # positive control first: a kernel whose checks fail on purpose is seen
+        lib = _lib.load()
+        lib.knnd_internal_check_selftest.argtypes = [C.c_void_p]
+        assert lib.knnd_internal_check_selftest(None) == 0
+        assert lib.knnd_check_failures(C.byref(cnt), C.byref(first)) == 0, _lib.last_error()
+        print(f"self-test: {cnt.value} failures reported, first at {first.value}", flush=True)
+        assert cnt.value == 2 and first.value // 100000 == 9, (cnt.value, first.value)
+        rc = _lib.load().knnd_check_failures(C.byref(cnt), C.byref(first))
+        assert rc == 0, _lib.last_error()
+        print(f"device bounds checks failed: {cnt.value} (first at file*100000+line {first.value})", flush=True)
+        assert cnt.value == 0, f"{cnt.value} device bounds checks failed, first at {first.value}"
 
 
 if __name__ == "__main__":
