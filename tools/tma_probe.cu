@@ -19,7 +19,13 @@
     }                                                                                       \
   } while (0)
 
-constexpr int LD = 20;
+#ifndef PROBE_CP
+#define PROBE_CP "cp.async.cg"
+#endif
+#ifndef PROBE_LD
+#define PROBE_LD 20
+#endif
+constexpr int LD = PROBE_LD;
 constexpr int WARPS = 4;
 
 __device__ __forceinline__ unsigned su32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -88,7 +94,7 @@ __global__ void __launch_bounds__(WARPS * 32) stage_kernel(const __grid_constant
         const int r = r0 + t * RPI;
         const int y = __shfl_sync(0xffffffffu, my, r & 31);
         if (r0 < RPI && r < 32)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(st + r * LD + part * 4)),
+          asm volatile(PROBE_CP ".shared.global [%0], [%1], 16;" ::"r"(su32(st + r * LD + part * 4)),
                        "l"(tab + (size_t)y * LD + part * 4)
                        : "memory");
       }
@@ -130,7 +136,7 @@ int main(int argc, char **argv) {
   const int batches = argc > 2 ? atoi(argv[2]) : 256;
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-  const int blocks_per_sm = 4;
+  const int blocks_per_sm = argc > 4 ? atoi(argv[4]) : 4;
   const int grid = sms * blocks_per_sm;
   const long nw = (long)grid * WARPS;
   float *tab;
