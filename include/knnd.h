@@ -104,6 +104,7 @@ int knnd_csr_build(const int32_t *friends, int64_t n, int32_t k, int64_t row_lo,
  *   tally[1] += #rows that differ from friends[x] (order-sensitive,
  *               RoundStats.changed_friend_sets, descent.py:276-277)
  *   tally[2] += #anchors with |U_x| < K (malformed input; must stay 0)
+ *   tally[3] += #rows whose order the screen could not certify (ranked in fp64)
  *   (tally is 4 x uint64, device memory, accumulated — the caller zeroes it)
  * max_indeg must be >= the longest CSR segment (from knnd_csr_build).
  * bound_in / bound_out (nullable, row_hi-row_lo floats): a per-row bound kept
@@ -140,6 +141,12 @@ int knnd_local_join(const double *points, const float *log32, const double *log6
  * memory over NVLink).  The stores overlap the join; before any rank reads the
  * gathered table, the caller runs a cross-rank barrier on the stream (the
  * kernels end with a system-scope fence).  npeers in 0..KNND_MAX_PEERS.
+ * q15 / q15_h / ld16 (nullable q15): screen with the 15-bit fixed-point log
+ * table of knnd_kl_q15_prepare instead of log32 (rows of ld16 = 16 or 24
+ * entries, K <= 32) — for tables larger than L2, where the random row gather
+ * is DRAM-bound and 48-byte rows move faster than 80-byte ones; the error
+ * bound widens to the quantisation step and the fp64 decision is unchanged,
+ * so results do not depend on it.
  * side_stream (nullable, a stream of the same device other than `stream`):
  * the few long anchors of the big-table size classes run there, concurrently
  * with the bulk classes on `stream`; the call forks to it and joins back, so
@@ -154,7 +161,20 @@ int knnd_local_join_peers(const double *points, const float *log32, const double
                           int32_t *out_ucount, unsigned long long *tally,
                           const float *bound_in, float *bound_out, void *ws, size_t ws_bytes,
                           uint32_t flags, int32_t *const *peer_tables, int32_t npeers,
-                          void *stream, void *side_stream);
+                          const uint16_t *q15, const float *q15_h, int32_t ld16, void *stream,
+                          void *side_stream);
+
+/*
+ * The 15-bit fixed-point copy of the log table for the join's q15 screen:
+ * per column j, L0_j = min log, h_j = (max log - L0_j) / 32767 (0 for a
+ * constant column), q = round((log64 - L0_j) / h_j) in 0..32767, stored as
+ * 0x8000 | q in rows of ld16 entries (ld16 % 8 == 0, >= d; padding 0x8000);
+ * qh[j] = (float)h_j (ld16 floats, 0 past d).  |log - (L0_j + h_j q)| <= h_j / 2.
+ * Workspace: knnd_kl_q15_workspace_bytes(d).
+ */
+size_t knnd_kl_q15_workspace_bytes(int32_t d);
+int knnd_kl_q15_prepare(const double *log64, int64_t n, int32_t d, int32_t ld16, uint16_t *q15,
+                        float *qh, void *ws, size_t ws_bytes, void *stream);
 
 /*
  * Friend clustering rate count — friend_clustering_rate (descent.py:317-338)

@@ -39,7 +39,9 @@ _SIGS = {
     "knnd_local_join": ([_P, _P, _P, _P, _I64, _I32, _I32, _P, _I32, _P, _P, _I64, _I64, _I32, _P, _P, _P, _P,
                          _P, _P, _P, _SZ, C.c_uint32, _P], C.c_int),
     "knnd_local_join_peers": ([_P, _P, _P, _P, _I64, _I32, _I32, _P, _I32, _P, _P, _I64, _I64, _I32, _P, _P, _P,
-                               _P, _P, _P, _P, _SZ, C.c_uint32, _P, _I32, _P, _P], C.c_int),
+                               _P, _P, _P, _P, _SZ, C.c_uint32, _P, _I32, _P, _P, _I32, _P, _P], C.c_int),
+    "knnd_kl_q15_workspace_bytes": ([_I32], _SZ),
+    "knnd_kl_q15_prepare": ([_P, _I64, _I32, _I32, _P, _P, _P, _SZ, _P], C.c_int),
     "knnd_fcc": ([_P, _I64, _I32, _P, _P, _P, _I32, _P, _P], C.c_int),
     "knnd_sort_rows": ([_P, _P, _P, _I64, _I32, _I32, _I64, _I64, _P, _P, _P, _P], C.c_int),
     "knnd_exact_knn_workspace_bytes": ([_I64, _I32, _I64, _I32], _SZ),

@@ -58,6 +58,9 @@ struct JoinParams {
   int d, ld, K;
   float band;
   int nonpos;  // every log coordinate <= 0: sum |x log y| == -sum x log y exactly
+  const float *__restrict__ qh;  // Q15 screen: per-column steps h_j (log32 then points at the q15 rows)
+  int nvq;                       // Q15: 16-byte chunks per q15 row
+  const float *__restrict__ l32;  // Q15: the fp32 log rows (the second screening tier of R)
   const float *__restrict__ bound_in;  // per own row: max screened value of the current row (or NaN)
   float *__restrict__ bound_out;       // the same for the row written this round
   // metric (score.cuh): KL, or squared Euclidean (EuclideanRankingSystem, similarity.py:119-140)
@@ -309,6 +312,53 @@ __device__ __forceinline__ void screen_row_reg(const float *row, const float4 (&
   ab = b;
 }
 
+// ---------------------------------------------------------------------------
+// The 15-bit fixed-point screen (Q15: tables larger than L2, where the random
+// row gather runs at DRAM speed and the row's byte count sets the rate; rows
+// of 8*NV4 entries of 0x8000 | q, knnd_kl_q15_prepare).  With log y_j =
+// L0_j + h_j q_j + e_j (|e_j| <= h_j / 2) and F_j = 1 + q_j 2^-15 (built
+// exactly from the stored half-word by one byte permute), the screened value
+// v = -sum_j w_j F_j, w_j = x_j h_j 2^15, equals the cross entropy minus a
+// per-anchor constant (2^15 sum_j x_j h_j - sum_j x_j L0_j) minus sum_j x_j e_j.
+// The error bound per anchor: A1 = sum_j |x_j| h_j;
+//   quantisation            A1 / 2
+//   fp32 weights and FMAs   (8 NV4 + 4) 2^-23 * sum_j |w_j F_j| <= (8 NV4 + 4) 2^-23 * 2^16 A1
+// so eb = A1 (1/2 + (8 NV4 + 4) 2^-7), generously; screened values of one
+// anchor then obey |v - (ce - const)| <= eb, which takes the place of
+// band * am + slack in the threshold and certification rules.
+template <int NV4>
+__device__ __forceinline__ float q15_weights(const double *x64, const float *__restrict__ qh, int d,
+                                             float (&w)[8 * NV4]) {
+  float a1 = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8 * NV4; ++j) {
+    const float x = j < d ? (float)x64[j] : 0.f;
+    const float h = j < d ? __ldg(qh + j) : 0.f;
+    w[j] = x * h * 32768.f;
+    a1 = fmaf(fabsf(x), h, a1);
+  }
+  return a1 * (1.f + 0x1p-16f) * (0.5f + (8 * NV4 + 4) * 0x1p-7f);
+}
+
+template <int NV4>
+__device__ __forceinline__ float screen_row_q15(const float *row, const float (&w)[8 * NV4]) {
+  const uint4 *r4 = reinterpret_cast<const uint4 *>(row);
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+  for (int q = 0; q < NV4; ++q) {
+    const uint4 u = r4[q];
+    a0 = fmaf(w[8 * q + 0], __uint_as_float(__byte_perm(u.x, 0x3F000000u, 0x7104)), a0);
+    a1 = fmaf(w[8 * q + 1], __uint_as_float(__byte_perm(u.x, 0x3F000000u, 0x7324)), a1);
+    a2 = fmaf(w[8 * q + 2], __uint_as_float(__byte_perm(u.y, 0x3F000000u, 0x7104)), a2);
+    a3 = fmaf(w[8 * q + 3], __uint_as_float(__byte_perm(u.y, 0x3F000000u, 0x7324)), a3);
+    a0 = fmaf(w[8 * q + 4], __uint_as_float(__byte_perm(u.z, 0x3F000000u, 0x7104)), a0);
+    a1 = fmaf(w[8 * q + 5], __uint_as_float(__byte_perm(u.z, 0x3F000000u, 0x7324)), a1);
+    a2 = fmaf(w[8 * q + 6], __uint_as_float(__byte_perm(u.w, 0x3F000000u, 0x7104)), a2);
+    a3 = fmaf(w[8 * q + 7], __uint_as_float(__byte_perm(u.w, 0x3F000000u, 0x7324)), a3);
+  }
+  return -((a0 + a1) + (a2 + a3));
+}
+
 // issue cp.async copies of the fp64 log rows of ids[0..nrow) into stage
 // (row stride sd doubles, sd odd to spread banks), 8 B chunks
 __device__ __forceinline__ void stage_rows_f64(double *stage, int sd, const double *__restrict__ log64,
@@ -432,6 +482,29 @@ __device__ __forceinline__ bool certify_row(const JoinParams &p, const int32_t *
   return true;
 }
 
+// The Q15 screen's second tier: when its (wider) bound cannot certify R's
+// order, rescreen the members of R (<= 32) with their fp32 log rows — the
+// fp32 bound of the local join, ~100x tighter — and certify that order; the
+// fp64 ranking runs only if this fails too.  `vals` (R's screened values) are
+// overwritten; the row bound stays theta (it must be in Q15 units).
+__device__ __forceinline__ bool certify_row_f32(const JoinParams &p, const int32_t *ids, float *vals, int nR,
+                                                float *stage, const float *x32, int x, int64_t xr, int lane,
+                                                bool &diff) {
+  const int ld = p.ld;  // the fp32 row length
+  stage_rows_f32<0>(stage, p.l32, ids, nR, ld, lane);
+  cp_async_wait_all();
+  __syncwarp();
+  float ce = __int_as_float(0x7f800000), ab = 0.f;
+  if (lane < nR) screen_row<0>(stage + lane * ld, x32, ld, p.nonpos, ce, ab);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ab = fmaxf(ab, __shfl_xor_sync(FULL, ab, o));
+  __syncwarp();
+  if (lane < nR) vals[lane] = ce;
+  __syncwarp();
+  float kth_unused;
+  return certify_row(p, ids, vals, nR, 2.f * p.band * ab, x, xr, lane, diff, kth_unused);
+}
+
 // ---------------------------------------------------------------------------
 // block-per-anchor kernel (classes B and L)
 
@@ -540,7 +613,7 @@ __device__ __forceinline__ void hist_find(const int *hist, int target, int *hdr,
   }
 }
 
-template <int G, int NV4, int KPL, bool GTAB, bool PF>
+template <int G, int NV4, int KPL, bool GTAB, bool PF, bool Q15>
 __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__restrict__ alist,
                                                  const int32_t *__restrict__ acount, int logH, int SW,
                                                  int32_t *__restrict__ gslab, int64_t slab_ints) {
@@ -564,7 +637,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     slabS = slab;
     table = slab + SW;
     list = table + H;
-    wrows = min(32, lstage_floats(p.ld) / (2 * p.ld));  // rows per buffer, two buffers per warp
+    wrows = min(32, lstage_floats(p.ld) / (2 * (Q15 ? NV4 * 4 : p.ld)));  // rows per buffer, two buffers per warp
     wstage = reinterpret_cast<float *>(sm + L.stage) + (size_t)warp * lstage_floats(p.ld);
     stage64 = reinterpret_cast<double *>(sm + L.stage);
     rcap64 = 32;
@@ -577,10 +650,11 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     rcap64 = min(32, (2 * H) / ((p.d64 | 1) * 8));
   }
   const int K = p.K, K1 = K + 1;
-  const int d = p.d, ld = p.ld;
+  const int d = p.d;
+  const int ld = Q15 ? NV4 * 4 : p.ld;  // staged row stride (floats): the q15 rows are 16 * NV4 bytes
   const int Gq = G / K1, Gr = G % K1;
   const int s_init = tid / K1, j_init = tid % K1;
-  unsigned long long acc_comp = 0, acc_changed = 0, acc_bad = 0;
+  unsigned long long acc_comp = 0, acc_changed = 0, acc_bad = 0, acc_exact = 0;
   const int count = *acount;
   int *cursor = const_cast<int *>(acount) + 8;  // dynamic anchor fetch (zeroed with the counts)
   // The next anchor is fetched one anchor ahead: thread 0 takes its index at the
@@ -668,7 +742,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
       for (int i = tid; i < nS; i += G)
         S[i] = i < K ? __ldg(p.F + (int64_t)x * K + i) : __ldg(p.indices + c0 + (i - K));
     if (!p.aside32)
-      for (int i = tid; i < ld; i += G) x32[i] = i < d ? (float)x64[i] : 0.f;
+      for (int i = tid; i < p.ld; i += G) x32[i] = i < d ? (float)x64[i] : 0.f;
     if (tid == 0) {
       hdr[0] = 0;
       hdr[1] = 0;
@@ -804,8 +878,12 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     float mn = __int_as_float(0x7f800000), mx = -mn, am = 0.f;
     const float slack = p.slack;
     float best0 = mn, best1 = mn;  // this lane's two smallest screened values
-    float4 xreg[NV4 > 0 ? NV4 : 1];  // the anchor's fp32 row in registers
-    if constexpr (NV4 > 0) {
+    float4 xreg[NV4 > 0 && !Q15 ? NV4 : 1];  // the anchor's fp32 row in registers
+    float wq[Q15 ? 8 * NV4 : 1];               // Q15: the anchor's weights
+    float eb = 0.f;                             // Q15: the per-anchor screen error bound
+    if constexpr (Q15) {
+      eb = q15_weights<NV4>(x64, p.qh, d, wq);
+    } else if constexpr (NV4 > 0) {
 #pragma unroll
       for (int q = 0; q < NV4; ++q) xreg[q] = reinterpret_cast<const float4 *>(x32)[q];
     }
@@ -843,10 +921,14 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
         const bool in = rr < nrow;
         const int rl = in ? rr : 0;
         float ce, ab;
-        if constexpr (NV4 > 0)
+        if constexpr (Q15) {
+          ce = screen_row_q15<NV4>(wstage + buf * wrows * ld + rl * ld, wq);
+          ab = 0.f;
+        } else if constexpr (NV4 > 0) {
           screen_row_reg<NV4>(wstage + buf * wrows * ld + rl * ld, xreg, p.nonpos, ce, ab);
-        else
+        } else {
           screen_row<NV4>(wstage + buf * wrows * ld + rl * ld, x32, ld, p.nonpos, ce, ab);
+        }
         if (in) {
           scores[k0 + rl] = ce;
           mn = fminf(mn, ce);
@@ -882,7 +964,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
         float ab = 0.f;
 #pragma unroll
         for (int w = 0; w < W; ++w) ab = fmaxf(ab, red[w * 4 + 2]);
-        const float th0 = T0 + 2.f * (p.band * ab + slack) + fabsf(T0) * 1e-6f;
+        const float th0 = T0 + 2.f * (Q15 ? eb : p.band * ab + slack) + fabsf(T0) * 1e-6f;
         collect_r(scores, list, U, th0, R, rval, &hdr[1], tid, lane, G);
         __syncthreads();
         if (hdr[1] <= 32) {
@@ -965,7 +1047,8 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
         T += (fabsf(T) + range) * 1e-6f;  // covers the rounding of t and of this line
       }
     }
-    const float theta = T + 2.f * (p.band * am + slack) + fabsf(T) * 1e-6f;
+    const float ebase = Q15 ? eb : p.band * am + slack;  // the screen's error bound at this anchor
+    const float theta = T + 2.f * ebase + fabsf(T) * 1e-6f;
     if (hdr[8] < count) prefetch(pb ^ 1, hdr[9], hdr64[0], hdr[12]);
 
     // ---- phase 3: collect every candidate the screen cannot exclude
@@ -980,8 +1063,10 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
       bool diff;
       float kth = theta;  // every member of the new row has a screened value <= theta
       if (!(KPL == 1 && p.out_kl == nullptr && nR <= 32 &&
-            certify_row(p, R, rval, nR, 2.f * (p.band * am + slack), x, xr, lane, diff, kth))) {
+            (certify_row(p, R, rval, nR, 2.f * ebase, x, xr, lane, diff, kth) ||
+             (Q15 && certify_row_f32(p, R, rval, nR, reinterpret_cast<float *>(stage64), x32, x, xr, lane, diff))))) {
         diff = exact_row<KPL>(p, R, nR, stage64, rcap64, x64, x, xr, lane);
+        ++acc_exact;
       }
       if (p.bound_out && lane == 0) p.bound_out[xr] = kth;
       if (lane == 0) {
@@ -1001,6 +1086,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     if (acc_comp) atomicAdd(&p.tally[0], acc_comp);
     if (acc_changed) atomicAdd(&p.tally[1], acc_changed);
     if (acc_bad) atomicAdd(&p.tally[2], acc_bad);
+    if (acc_exact) atomicAdd(&p.tally[3], acc_exact);
   }
 }
 
@@ -1054,7 +1140,7 @@ __device__ __forceinline__ void prefetch_anchor(const JoinParams &p, int x, int6
   cp_async_commit();
 }
 
-template <int NV4, int KPL, bool VF>
+template <int NV4, int KPL, bool VF, bool Q15>
 __global__ void __launch_bounds__(128, 4)
     join_warp_kernel(JoinParams p, const int32_t *__restrict__ alist, const int32_t *__restrict__ acount, int logH,
                      int SW) {
@@ -1077,11 +1163,12 @@ __global__ void __launch_bounds__(128, 4)
   float *scores = reinterpret_cast<float *>(table);            // phase 2-3: [0, U)
   double *stage64 = reinterpret_cast<double *>(table);         // phase 4: whole table
   const int K = p.K, K1 = K + 1;
-  const int d = p.d, ld = p.ld, sd = p.d64 | 1;
+  const int d = p.d, sd = p.d64 | 1;
+  const int ld = Q15 ? NV4 * 4 : p.ld;  // staged row stride (floats): the q15 rows are 16 * NV4 bytes
   const int rcap64 = min(32, (4 * H) / (sd * 8));
   const int Gq = 32 / K1, Gr = 32 % K1;
   const int s_init = lane / K1, j_init = lane % K1;
-  unsigned long long acc_comp = 0, acc_changed = 0, acc_bad = 0;
+  unsigned long long acc_comp = 0, acc_changed = 0, acc_bad = 0, acc_exact = 0;
   const int count = *acount;
   int *cursor = const_cast<int *>(acount) + 8;  // dynamic anchor fetch, 4 anchors per atomic
   // The next anchor is known one anchor ahead: its id is loaded when the
@@ -1134,10 +1221,14 @@ __global__ void __launch_bounds__(128, 4)
     cp_async_wait_all();  // this anchor's prefetched inputs
     __syncwarp();
     if (!p.aside32)
-      for (int i = lane; i < ld; i += 32) x32[i] = i < d ? (float)x64[i] : 0.f;
+      for (int i = lane; i < p.ld; i += 32) x32[i] = i < d ? (float)x64[i] : 0.f;
     __syncwarp();
-    float4 xreg[NV4 > 0 ? NV4 : 1];  // the anchor's fp32 row in registers
-    if constexpr (NV4 > 0) {
+    float4 xreg[NV4 > 0 && !Q15 ? NV4 : 1];  // the anchor's fp32 row in registers
+    float wq[Q15 ? 8 * NV4 : 1];               // Q15: the anchor's weights
+    float eb = 0.f;                             // Q15: the per-anchor screen error bound
+    if constexpr (Q15) {
+      eb = q15_weights<NV4>(x64, p.qh, d, wq);
+    } else if constexpr (NV4 > 0) {
 #pragma unroll
       for (int q = 0; q < NV4; ++q) xreg[q] = reinterpret_cast<const float4 *>(x32)[q];
     }
@@ -1298,10 +1389,14 @@ __global__ void __launch_bounds__(128, 4)
         const bool in = rr < nrow;
         const int rl = in ? rr : 0;  // lanes past nrow recompute row 0, discarded
         float ce, ab;
-        if constexpr (NV4 > 0)
+        if constexpr (Q15) {
+          ce = screen_row_q15<NV4>(stage + buf * rows * ld + rl * ld, wq);
+          ab = 0.f;
+        } else if constexpr (NV4 > 0) {
           screen_row_reg<NV4>(stage + buf * rows * ld + rl * ld, xreg, p.nonpos, ce, ab);
-        else
+        } else {
           screen_row<NV4>(stage + buf * rows * ld + rl * ld, x32, ld, p.nonpos, ce, ab);
+        }
         if (in) scores[k0 + rl] = ce;
         am = in ? fmaxf(am, ab) : am;
         float v = in ? ce : __int_as_float(0x7f800000);
@@ -1347,8 +1442,9 @@ __global__ void __launch_bounds__(128, 4)
       return t;
     };
     float T;
+    const float ebase = Q15 ? eb : p.band * am + slack;  // the screen's error bound at this anchor
     if (KPL == 1 && isfinite(T0)) {
-      const float th0 = T0 + 2.f * (p.band * am + slack) + fabsf(T0) * 1e-6f;
+      const float th0 = T0 + 2.f * ebase + fabsf(T0) * 1e-6f;
       int cnt = 0;
       for (int k0 = 0; k0 < U; k0 += 32) {
         const int k = k0 + lane;
@@ -1358,7 +1454,7 @@ __global__ void __launch_bounds__(128, 4)
     } else {
       T = lane_pair_T();
     }
-    const float theta = T + 2.f * (p.band * am + slack) + fabsf(T) * 1e-6f;
+    const float theta = T + 2.f * ebase + fabsf(T) * 1e-6f;
 
     // ---- phase 3: R (ids and screened values) in place at the front of list / scores
     int nR = 0;
@@ -1381,8 +1477,10 @@ __global__ void __launch_bounds__(128, 4)
     bool diff;
     float kth = theta;  // every member of the new row has a screened value <= theta
     if (!(KPL == 1 && p.out_kl == nullptr && nR <= 32 &&
-          certify_row(p, list, scores, nR, 2.f * (p.band * am + slack), x, xr, lane, diff, kth))) {
+          (certify_row(p, list, scores, nR, 2.f * ebase, x, xr, lane, diff, kth) ||
+           (Q15 && certify_row_f32(p, list, scores, nR, scores + 32, x32, x, xr, lane, diff))))) {
       diff = exact_row<KPL>(p, list, nR, stage64, rcap64, x64, x, xr, lane);
+      ++acc_exact;
     }
     if (p.bound_out && lane == 0) p.bound_out[xr] = kth;
     if (lane == 0) {
@@ -1404,6 +1502,7 @@ __global__ void __launch_bounds__(128, 4)
     if (acc_comp) atomicAdd(&p.tally[0], acc_comp);
     if (acc_changed) atomicAdd(&p.tally[1], acc_changed);
     if (acc_bad) atomicAdd(&p.tally[2], acc_bad);
+    if (acc_exact) atomicAdd(&p.tally[3], acc_exact);
   }
 }
 
@@ -1576,12 +1675,13 @@ static Plan make_plan(int64_t n_items, int64_t m, int d, int K, int max_indeg) {
   return P;
 }
 
-template <int G, int NV4, int KPL, bool GTAB>
+template <int G, int NV4, int KPL, bool GTAB, bool Q15 = false>
 static int launch_join(const JoinParams &p, const int32_t *alist, const int32_t *acount, int logH, int SW,
                        int32_t *gslab, int64_t slab_ints, int grid_cap, cudaStream_t st) {
   // friend ids two groups ahead pays for the larger shared tables (B128 at 2^13:
   // -8%); at 2^12 (at most 4 groups per anchor) it measured 20% slower
-  auto kern = (!GTAB && logH >= 13) ? join_kernel<G, NV4, KPL, GTAB, !GTAB> : join_kernel<G, NV4, KPL, GTAB, false>;
+  auto kern = (!GTAB && logH >= 13) ? join_kernel<G, NV4, KPL, GTAB, !GTAB, Q15>
+                                    : join_kernel<G, NV4, KPL, GTAB, false, Q15>;
   const SmemLayout L = smem_layout(G, GTAB, p.d, p.ld, 1 << logH, SW);
   const size_t smem = L.total;
   if (smem > 227 * 1024) {
@@ -1602,11 +1702,11 @@ static int launch_join(const JoinParams &p, const int32_t *alist, const int32_t 
   return KNND_OK;
 }
 
-template <int NV4, int KPL>
+template <int NV4, int KPL, bool Q15 = false>
 static int launch_warp(const JoinParams &p, const int32_t *alist, const int32_t *acount, int logH, int SW,
                        cudaStream_t st) {
   // friend rows as int4 when they are 16-B aligned (K % 4 == 0)
-  auto kern = (p.K % 4 == 0) ? join_warp_kernel<NV4, KPL, true> : join_warp_kernel<NV4, KPL, false>;
+  auto kern = (p.K % 4 == 0) ? join_warp_kernel<NV4, KPL, true, Q15> : join_warp_kernel<NV4, KPL, false, Q15>;
   const WarpSlab L = warp_slab(p.d, p.ld, 1 << logH, SW);
   // warps per block: the largest of 4/2/1 that keeps the most warps resident
   // (big tables leave room for fewer than 4 slabs per block slot)
@@ -1647,6 +1747,10 @@ static int launch_warp(const JoinParams &p, const int32_t *alist, const int32_t 
 template <int G, bool GTAB>
 static int dispatch_block(const Plan &P, const JoinParams &p, const int32_t *alist, const int32_t *acount,
                           int logH, int SW, int32_t *gslab, int64_t slab_ints, int grid_cap, cudaStream_t st) {
+  if (p.qh) {  // the Q15 screen (K <= 32, rows of 2 or 3 16-byte chunks; checked at the entry)
+    if (p.nvq == 2) return launch_join<G, 2, 1, GTAB, true>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st);
+    return launch_join<G, 3, 1, GTAB, true>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st);
+  }
 #define KNND_CALL(NV)                                                                                          \
   return P.kpl == 1 ? launch_join<G, NV, 1, GTAB>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st) \
                     : launch_join<G, NV, 2, GTAB>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st)
@@ -1656,6 +1760,10 @@ static int dispatch_block(const Plan &P, const JoinParams &p, const int32_t *ali
 
 static int dispatch_warp(const Plan &P, const JoinParams &p, const int32_t *alist, const int32_t *acount, int logH,
                          int SW, cudaStream_t st) {
+  if (p.qh) {
+    if (p.nvq == 2) return launch_warp<2, 1, true>(p, alist, acount, logH, SW, st);
+    return launch_warp<3, 1, true>(p, alist, acount, logH, SW, st);
+  }
 #define KNND_CALL(NV)                                                             \
   return P.kpl == 1 ? launch_warp<NV, 1>(p, alist, acount, logH, SW, st) \
                     : launch_warp<NV, 2>(p, alist, acount, logH, SW, st)
@@ -1822,8 +1930,8 @@ static int join_run(const char *who, JoinParams &p, int64_t n, int32_t dplan, in
       KNND_CUDA(cudaMemcpy(t1, tally, sizeof(t1), cudaMemcpyDeviceToHost));
       KNND_CUDA(cudaMemcpy(cnt, counts, sizeof(int) * P.ncls, cudaMemcpyDeviceToHost));
       const unsigned long long u = t1[0] - t0[0];
-      fprintf(stderr, "knnd class %d kind %d logH %d: %d anchors, %llu comparisons, %.3f ms, %.3e/s\n", i,
-              P.c[i].kind, P.c[i].logH, cnt[i], u, ms, ms > 0 ? u / (ms * 1e-3) : 0.0);
+      fprintf(stderr, "knnd class %d kind %d logH %d: %d anchors, %llu comparisons, %.3f ms, %.3e/s, %llu rows ranked in fp64\n",
+              i, P.c[i].kind, P.c[i].logH, cnt[i], u, ms, ms > 0 ? u / (ms * 1e-3) : 0.0, t1[3] - t0[3]);
       cudaEventDestroy(e0);
       cudaEventDestroy(e1);
     }
@@ -1857,7 +1965,7 @@ int knnd_local_join_peers(const double *points, const float *log32, const double
                           int32_t max_indeg, int32_t *out_ids, double *out_kl, int32_t *out_ucount,
                           unsigned long long *tally, const float *bound_in, float *bound_out, void *ws,
                           size_t ws_bytes, uint32_t flags, int32_t *const *peer_tables, int32_t npeers,
-                          void *stream, void *side_stream) {
+                          const uint16_t *q15, const float *q15_h, int32_t ld16, void *stream, void *side_stream) {
   KNND_CHECK_ARG(points && log32 && log64 && xlogx, "knnd_local_join: null pointer");
   JoinParams p{};
   p.points = points;
@@ -1880,6 +1988,15 @@ int knnd_local_join_peers(const double *points, const float *log32, const double
   p.d64 = d;
   p.pstride = d;
   p.aside32 = nullptr;
+  if (q15) {  // the 15-bit fixed-point screen (knnd_kl_q15_prepare)
+    KNND_CHECK_ARG(q15_h && (ld16 == 16 || ld16 == 24) && ld16 >= d && k <= 32,
+                   "knnd_local_join: the q15 screen needs q15_h, ld16 16 or 24 (>= d) and K <= 32 (ld16=%d K=%d)",
+                   ld16, k);
+    p.l32 = log32;
+    p.log32 = reinterpret_cast<const float *>(q15);
+    p.qh = q15_h;
+    p.nvq = ld16 / 8;
+  }
   if (int rc = set_peers(p, "knnd_local_join", peer_tables, npeers)) return rc;
   return join_run("knnd_local_join", p, n, d, k, row_lo, row_hi, max_indeg, ws, ws_bytes, stream, side_stream);
 }
@@ -1891,7 +2008,7 @@ int knnd_local_join(const double *points, const float *log32, const double *log6
                     float *bound_out, void *ws, size_t ws_bytes, uint32_t flags, void *stream) {
   return knnd_local_join_peers(points, log32, log64, xlogx, n, d, ld32, friends, k, indptr, indices, row_lo, row_hi,
                                max_indeg, out_ids, out_kl, out_ucount, tally, bound_in, bound_out, ws, ws_bytes, flags,
-                               nullptr, 0, stream, nullptr);
+                               nullptr, 0, nullptr, nullptr, 0, stream, nullptr);
 }
 
 int knnd_l2_local_join_peers(const float *anchor32, const float *cand32, const double *rows64, const double *sq64,

@@ -32,6 +32,60 @@ __global__ void kl_prepare_kernel(const double *__restrict__ pts, int64_t n, int
   }
 }
 
+// The 15-bit fixed-point log table of the join's screen for tables larger than
+// L2 (join.cu, Q15): per column j, L0_j = min log, h_j = (max - min) / 32767
+// (0 for a constant column), q = round((log - L0_j) / h_j), stored as
+// 0x8000 | q so that the screen builds the float 1 + q 2^-15 with one byte
+// permute.  |log - (L0_j + h_j q)| <= h_j / 2.  Rows of ld16 entries (zero
+// padded; 16-byte rows).  qh[j] = (float)h_j.
+__device__ __forceinline__ unsigned long long ord_f64(double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  return b ^ ((unsigned long long)((long long)b >> 63) | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double unord_f64(unsigned long long u) {
+  const unsigned long long b = u ^ ((unsigned long long)((long long)~u >> 63) | 0x8000000000000000ull);
+  return __longlong_as_double((long long)b);
+}
+
+__global__ void col_minmax_kernel(const double *__restrict__ log64, int64_t n, int d,
+                                  unsigned long long *__restrict__ mm) {  // [2d]: min, then max (ordered bits)
+  const int rows_per = blockDim.x / d;  // column j = thread % d of rows_per rows at a time
+  if ((int)threadIdx.x >= rows_per * d) return;
+  const int j = threadIdx.x % d;
+  unsigned long long lo = ~0ull, hi = 0ull;
+  for (int64_t r = (int64_t)blockIdx.x * rows_per + threadIdx.x / d; r < n; r += (int64_t)gridDim.x * rows_per) {
+    const unsigned long long u = ord_f64(log64[r * d + j]);
+    lo = u < lo ? u : lo;
+    hi = u > hi ? u : hi;
+  }
+  atomicMin(mm + j, lo);
+  atomicMax(mm + d + j, hi);
+}
+
+__global__ void q15_quantize_kernel(const double *__restrict__ log64, int64_t n, int d, int ld16,
+                                    const unsigned long long *__restrict__ mm, uint16_t *__restrict__ q15,
+                                    float *__restrict__ qh) {
+  const int64_t total = n * ld16;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / ld16;
+    const int j = (int)(i - r * ld16);
+    unsigned q = 0;
+    if (j < d) {
+      const double lo = unord_f64(mm[j]), hi = unord_f64(mm[d + j]);
+      const double h = (hi - lo) / 32767.0;
+      if (h > 0.0) {
+        double t = rint((log64[r * d + j] - lo) / h);
+        t = t < 0.0 ? 0.0 : (t > 32767.0 ? 32767.0 : t);
+        q = (unsigned)t;
+      }
+      if (r == 0) qh[j] = (float)h;
+    } else if (r == 0) {
+      qh[j] = 0.f;
+    }
+    q15[i] = (uint16_t)(0x8000u | q);
+  }
+}
+
 // core.py:97-103 / similarity.py:101-106 — exact scores of ids against anchor x
 // (L2: similarity.py:135-140, pts = log64 = the vector rows with |v|^2 appended)
 __global__ void batch_scores_kernel(const double *__restrict__ pts, int pstride, const double *__restrict__ log64,
@@ -216,6 +270,31 @@ int knnd_kl_prepare(const double *points, int64_t n, int32_t d, int32_t ld32, fl
   int64_t blocks = (n + 7) / 8;
   if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
   kl_prepare_kernel<<<(unsigned)blocks, threads, 0, as_stream(stream)>>>(points, n, d, ld32, log32, log64, xlogx);
+  KNND_LAUNCHED(1);
+  return KNND_OK;
+}
+
+size_t knnd_kl_q15_workspace_bytes(int32_t d) { return d < 1 ? 0 : align_up((size_t)d * 16, 256); }
+
+int knnd_kl_q15_prepare(const double *log64, int64_t n, int32_t d, int32_t ld16, uint16_t *q15, float *qh, void *ws,
+                        size_t ws_bytes, void *stream) {
+  KNND_CHECK_ARG(log64 && q15 && qh, "knnd_kl_q15_prepare: null pointer");
+  KNND_CHECK_ARG(n >= 1 && d >= 1 && d <= 256, "knnd_kl_q15_prepare: bad shape n=%lld d=%d", (long long)n, d);
+  KNND_CHECK_ARG(ld16 >= d && ld16 % 8 == 0, "knnd_kl_q15_prepare: ld16=%d must be >= d and a multiple of 8", ld16);
+  if (!ws || ws_bytes < knnd_kl_q15_workspace_bytes(d)) {
+    set_error("knnd_kl_q15_prepare: workspace %zu < %zu bytes", ws_bytes, knnd_kl_q15_workspace_bytes(d));
+    return KNND_EWORKSPACE;
+  }
+  cudaStream_t st = as_stream(stream);
+  unsigned long long *mm = static_cast<unsigned long long *>(ws);
+  KNND_CUDA(cudaMemsetAsync(mm, 0xFF, (size_t)d * 8, st));
+  KNND_CUDA(cudaMemsetAsync(mm + d, 0x00, (size_t)d * 8, st));
+  const int threads = (256 / d) * d > 0 ? (256 / d) * d : d;
+  col_minmax_kernel<<<num_sms() * 4, threads, 0, st>>>(log64, n, d, mm);
+  KNND_LAUNCHED(1);
+  int64_t blocks = (n * ld16 + 255) / 256;
+  if (blocks > (int64_t)num_sms() * 32) blocks = (int64_t)num_sms() * 32;
+  q15_quantize_kernel<<<(unsigned)blocks, 256, 0, st>>>(log64, n, d, ld16, mm, q15, qh);
   KNND_LAUNCHED(1);
   return KNND_OK;
 }

@@ -106,6 +106,9 @@ def upload(host: np.ndarray, device: torch.device) -> torch.Tensor:
     return out
 
 
+Q15_MIN_BYTES = 96 << 20  # fp32 screen tables above this (of a 126 MB L2) take the 15-bit screen
+
+
 def _dev(device) -> torch.device:
     if device is None and not torch.cuda.is_available():
         raise RuntimeError("no CUDA device: the B200 KL local join has no CPU fallback")
@@ -137,15 +140,32 @@ class DeviceTables:
         _lib.call("knnd_kl_prepare", self.points.data_ptr(), self.n, self.d, self.ld, self.log32.data_ptr(),
                   self.log64.data_ptr(), self.xlogx.data_ptr(), _stream(device))
         self.dplan = self.d  # the screen row width the join plans for
+        # the join's 15-bit screen for tables larger than L2 (knnd_kl_q15_prepare):
+        # the random row gather is DRAM-bound there and 48-byte rows move faster
+        # than 80-byte ones; results do not depend on it (KNND_Q15=0/1 forces it)
+        self.q15 = self.qh = None
+        self.ld16 = (self.d + 7) // 8 * 8
+        force = os.environ.get("KNND_Q15")
+        want = force == "1" or (force is None and self.n * self.ld * 4 > Q15_MIN_BYTES)
+        if want and self.ld16 in (16, 24):
+            self.q15 = torch.empty((self.n, self.ld16), dtype=torch.int16, device=device)
+            self.qh = torch.empty(self.ld16, dtype=torch.float32, device=device)
+            ws = torch.empty(max(int(_lib.load().knnd_kl_q15_workspace_bytes(self.d)), 256), dtype=torch.uint8,
+                             device=device)
+            _lib.call("knnd_kl_q15_prepare", self.log64.data_ptr(), self.n, self.d, self.ld16, self.q15.data_ptr(),
+                      self.qh.data_ptr(), ws.data_ptr(), ws.numel(), _stream(device))
+            torch.cuda.current_stream(device).synchronize()  # ws is a temporary
 
     # -- the kernel calls (one per ABI entry; the L2 tables provide the same methods)
     def join(self, table, k, csr, max_indeg, out_rows, tally, out_scores, out_ucount, bound_in, bound_out, ws,
              flags, stream, peers=(), side_stream=None):
+        q15 = self.q15 is not None and k <= 32  # (the same choice every round of a descent: K is fixed)
         _lib.call("knnd_local_join_peers", self.points.data_ptr(), self.log32.data_ptr(), self.log64.data_ptr(),
                   self.xlogx.data_ptr(), self.n, self.d, self.ld, table.data_ptr(), k, csr.indptr.data_ptr(),
                   csr.indices.data_ptr(), csr.lo, csr.hi, max_indeg, out_rows.data_ptr(), _ptr(out_scores),
                   _ptr(out_ucount), tally.data_ptr(), _ptr(bound_in), _ptr(bound_out), ws.data_ptr(), ws.numel(),
-                  flags, _lib.peer_array(peers), len(peers), stream, side_stream)
+                  flags, _lib.peer_array(peers), len(peers), _ptr(self.q15) if q15 else None,
+                  _ptr(self.qh) if q15 else None, self.ld16 if q15 else 0, stream, side_stream)
 
     def join_flags(self) -> int:
         return _lib.JOIN_NONPOS_LOG if self.max_coord <= 1.0 else 0
