@@ -374,6 +374,27 @@ def test_c4_trajectory(cuda, trajectories):
         _recall_check("c4", pts, final, rec, 10_000)
 
 
+@pytest.mark.slow
+def test_c5_trajectory(cuda, trajectories):
+    """C5, n = 10M, d = 20, K = 20 (the scaling-stress config, 800 MB fp32 log
+    table, the Q15 screen): the initial table and both rounds' tables equal
+    the reference's recorded ones (sha256), with its comparisons, changed rows
+    and FCC counts, and the descent stops at the same round (2).  Recall of the
+    final table on the reference's 10,000-id sample, exact rows by the GPU
+    brute force, equals the reference's (computed with the C oracle)."""
+    from conftest import load_json
+
+    if "c5" not in trajectories:
+        pytest.skip("C5 trajectory not recorded")
+    pts, final = _trajectory_check(trajectories, "c5")
+    rec = load_json("recall.json")
+    if "c5" in rec:
+        rs = b2.KlRankingSystem(pts, validate=False)
+        sample = b2.uniform_recall_sample(pts.shape[0], 0, 10_000)
+        got = b2.sampled_recall(final, rs, sample)
+        assert abs(got - rec["c5"]["recall"]) <= 0.005, (got, rec["c5"])
+
+
 _SIDE_SCRIPT = r"""
 import sys, hashlib
 sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
