@@ -55,7 +55,7 @@ CONFIGS = {
 }
 # recall@K of the reference's own final tables on uniform_recall_sample(n, 0, 10000)
 # (tests/golden/recall.json, recorded from the reference's runs)
-REF_RECALL = {"c1": 0.99382, "c2": 0.9738, "c3": 0.617925, "c4": 0.3055466666666667}
+REF_RECALL = {"c1": 0.99382, "c2": 0.9738, "c3": 0.617925, "c4": 0.3055466666666667, "c5": 0.001455}
 CPU_SAMPLE_ANCHORS = 10_000_000  # i.e. every anchor of round 1 (bounded by n)
 
 
