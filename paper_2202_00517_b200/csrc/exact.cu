@@ -402,21 +402,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1) exact_tc_kernel(TcParams p) {
       const uint32_t col0 = (uint32_t)(2 * acc * TC_BN);
       // warp-uniform: does this tile hold padding columns or any of the warp's queries?
       const bool edge = __any_sync(FULL, y0 + TC_BN > p.n || (qid >= y0 && qid < y0 + TC_BN));
+      // columns of chunk c that never rank: the query itself and padding past n
+      // (32-bit masks, computed on the rare edge tiles only)
+      auto edge_mask = [&](int c) -> unsigned {
+        const int64_t yc = y0 + c * 32;
+        unsigned em = 0;
+        const int64_t sc = qid - yc;
+        if (sc >= 0 && sc < 32) em |= 1u << (int)sc;
+        const int64_t nv = p.n - yc;
+        if (nv < 32) em |= nv <= 0 ? ~0u : (~0u << (int)nv);
+        return em;
+      };
       if (!sweep2) {
         // sweep 1 (every TC_SUB1-th tile): slot minima, chunk c of tile t -> slot
-        // group (c + 4t) % SL; one chunk in flight keeps the minima in registers
-#pragma unroll
-        for (int c = 0; c < TC_BN / 32; ++c) {
-          uint32_t rv[32];
-          tc_ld32(lane_base + col0 + c * 32, rv);
-          tc_ld_wait(rv);
-          if (edge) {
-            const int64_t yc = y0 + c * 32;
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (yc + i >= p.n || yc + i == qid) rv[i] = 0x7f800000u;
-          }
-          if (SL == 4 && (t & 1)) {  // groups 2, 3 on odd tiles (static register indices)
+        // group c % SL (SL = 4: (c + 2) % 4 on odd tiles); one chunk in flight
+        // keeps the minima in registers.  Edge tiles take their own loop, so the
+        // masking never runs (predicated) on the others.
+        auto fold = [&](int c, const uint32_t(&rv)[32]) {
+          if (SL == 4 && (t & 1)) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const int j = ((c + 2) % SL) * 32 + i;
@@ -429,21 +432,38 @@ __global__ void __launch_bounds__(TC_THREADS, 1) exact_tc_kernel(TcParams p) {
               best[j] = fminf(best[j], __uint_as_float(rv[i]));
             }
           }
+        };
+        if (!edge) {
+#pragma unroll
+          for (int c = 0; c < TC_BN / 32; ++c) {
+            uint32_t rv[32];
+            tc_ld32(lane_base + col0 + c * 32, rv);
+            tc_ld_wait(rv);
+            fold(c, rv);
+          }
+        } else {
+#pragma unroll 1
+          for (int c = 0; c < TC_BN / 32; ++c) {
+            uint32_t rv[32];
+            tc_ld32(lane_base + col0 + c * 32, rv);
+            tc_ld_wait(rv);
+            const unsigned em = edge_mask(c);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) rv[i] = (em >> i) & 1u ? 0x7f800000u : rv[i];
+            if (c == 0) fold(0, rv);
+            else if (c == 1) fold(1, rv);
+            else if (c == 2) fold(2, rv);
+            else fold(3, rv);
+          }
         }
       } else {
         // sweep 2: append every column with ce <= theta (a 3-input min tree per
-        // chunk; the rare hits are walked through a bit mask)
+        // chunk; the rare hits are walked through a bit mask, minus the edge mask)
 #pragma unroll
         for (int c = 0; c < TC_BN / 32; ++c) {
           uint32_t rv[32];
           tc_ld32(lane_base + col0 + c * 32, rv);
           tc_ld_wait(rv);
-          const int64_t yc = y0 + c * 32;
-          if (edge) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (yc + i >= p.n || yc + i == qid) rv[i] = 0x7f800000u;
-          }
           float m[11];
 #pragma unroll
           for (int i = 0; i < 10; ++i)
@@ -452,10 +472,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) exact_tc_kernel(TcParams p) {
           const float mm = tc_min3(tc_min3(tc_min3(m[0], m[1], m[2]), tc_min3(m[3], m[4], m[5]),
                                            tc_min3(m[6], m[7], m[8])),
                                    m[9], m[10]);
-          if (mm <= theta) {  // rare: ~K..3K hits per query over all candidates
+          if (mm <= theta) {  // rare: ~K..3K hits per query over all candidates (and the self tile)
             unsigned hit = 0;
 #pragma unroll
             for (int i = 0; i < 32; ++i) hit |= (__uint_as_float(rv[i]) <= theta ? 1u : 0u) << i;
+            if (edge) hit &= ~edge_mask(c);
+            const int64_t yc = y0 + c * 32;
             while (hit) {
               const int i = __ffs(hit) - 1;
               hit &= hit - 1;
