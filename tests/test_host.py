@@ -226,3 +226,38 @@ def test_verify_total_order():
     rs = _LineRanking([0.0, 1.0, -1.0, 3.0, 2.5])
     assert b2.verify_total_order(rs, 0, range(5))
     assert not b2.verify_total_order(_Cyclic(), 5, [0, 1, 2])
+
+
+def test_fused_exchange_states_never_alias_a_reused_table(small_meta):
+    """The ping-pong tables of the fused exchange are reused every other round
+    (and by the next descent): a state handed to on_round raises once a later
+    round has overwritten its table (instead of silently showing another
+    table), and the final state is a private copy (engine.PeerTables.gen,
+    KnnState._detach)."""
+    import torch
+
+    from cpu_ops import CpuOps
+    from oracle import native
+    from paper_2202_00517_b200.descent import descend_resident, draw_fcc_schedule
+    from paper_2202_00517_b200.engine import Engine, PeerTables
+
+    meta = small_meta["n1000_d20_k20_s1"]
+    n, d, k, seed = meta["n"], meta["d"], meta["k"], meta["seed"]
+    pts = b2.sample_simplex_uniform(d, n, b2.derive_rng(seed, 1, d))
+    cfg = b2.DescentConfig(k=k, seed=seed)
+    rounds = cfg.resolved_max_rounds(n)
+    eng = Engine(n, k, torch.device("cpu"), ops=CpuOps())
+    bufs = [eng.alloc_table() for _ in range(2)]
+    assert eng.enable_peer_exchange(PeerTables(bufs, [[], []], lambda i: None))
+    table = eng.alloc_table()
+    eng.upload_rows(b2.random_kout_draws(n, k, b2.derive_rng(seed, 2)), table)
+    seen = []
+    state, hist = descend_resident(eng, native.Tables(pts), table, torch.from_numpy(draw_fcc_schedule(n, k, cfg, rounds)),
+                                   cfg.fcc_sample_count, rounds, on_round=lambda st, s: seen.append(st))
+    assert sha_i32(state.friends) == meta["rounds"][-1]["sha"]
+    assert all(state._table.data_ptr() != b.data_ptr() for b in bufs)  # the final table is private
+    assert len(seen) == len(hist) >= 3
+    seen[-1]._table  # the last round's table was not reused
+    for st in seen[:-2]:  # tables overwritten two rounds later
+        with pytest.raises(RuntimeError, match="reused by a later round"):
+            st.friends
