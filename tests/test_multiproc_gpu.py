@@ -1,5 +1,5 @@
-"""The row-sharded, fused-exchange path with the real CUDA kernels, 2 and 3
-ranks as processes sharing one GPU.
+"""The row-sharded, fused-exchange path with the real CUDA kernels, 2, 3, 4
+and 8 ranks as processes sharing one GPU (P = 1, 2, 4, 8 agree).
 
 Each rank is its own process on cuda:0 with its own copy of the tables.  The
 two ping-pong next tables of every rank are exported with CUDA IPC and opened
@@ -113,7 +113,7 @@ def _expect(meta):
     return [(r["comparisons"], r["changed"], r["fcc"]) for r in meta["rounds"]]
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 def test_fused_exchange_small_case(cuda, small_meta, world):
     meta = small_meta["n1000_d20_k20_s1"]
     res = _run(world, meta)
@@ -124,7 +124,7 @@ def test_fused_exchange_small_case(cuda, small_meta, world):
         assert res[rank]["launches"] > 0
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 def test_fused_exchange_c2_trajectory(cuda, trajectories, world):
     """C2 (n = 100k, d = 10, K = 20): every round's table on every rank equals the
     reference's recorded table (sha256), with the reference's tallies."""
