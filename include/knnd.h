@@ -5,10 +5,13 @@
  * One shared object, libknnd.so, built for sm_100a.  Every entry point takes
  * plain device pointers, sizes and a CUDA stream (passed as void*), is
  * stream-ordered, allocates no device memory and keeps no state apart from a
- * per-thread last-error string and a launch counter: streams are the
- * caller's, and the only CUDA objects the library creates are the two fork /
- * join events of one *_local_join_peers call with a side stream, destroyed
- * before that call returns.  The caller (the Python host in
+ * per-thread last-error string, a launch counter and a memo of launch
+ * configurations (per device and kernel: the dynamic-shared-memory limit set
+ * and the occupancy at a block shape — host data only, so repeated calls make
+ * no attribute or occupancy API calls): streams are the caller's, and the
+ * only CUDA objects the library creates are the two fork / join events of one
+ * *_local_join_peers call with a side stream, destroyed before that call
+ * returns.  The caller (the Python host in
  * paper_2202_00517_b200/, using PyTorch for device buffers) owns all memory.
  * Environment variables read per call (diagnostics / A-B only; results never
  * depend on them): KNND_PLAN, KNND_SIDE_CLASSES, KNND_CLASS_TIMING.

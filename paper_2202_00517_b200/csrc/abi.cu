@@ -2,6 +2,8 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <mutex>
+#include <unordered_map>
 
 #include "common.cuh"
 
@@ -18,6 +20,59 @@ void set_error(const char *fmt, ...) {
 }
 
 void count_launch(unsigned n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+namespace {
+struct OccKey {
+  int dev, block;
+  const void *kern;
+  size_t smem;
+  bool operator==(const OccKey &o) const {
+    return dev == o.dev && block == o.block && kern == o.kern && smem == o.smem;
+  }
+};
+struct OccKeyHash {
+  size_t operator()(const OccKey &k) const {
+    return std::hash<const void *>()(k.kern) ^ (std::hash<size_t>()(k.smem) * 31) ^ ((size_t)k.block << 20) ^
+           ((size_t)k.dev << 40);
+  }
+};
+std::mutex g_occ_mu;
+std::unordered_map<OccKey, int, OccKeyHash> g_occ;                      // -> blocks per SM
+std::unordered_map<const void *, size_t> g_smem_attr[64];               // per device: the smem limit set
+}  // namespace
+
+int kernel_occupancy(const void *kern, int block, size_t smem, int *per_sm) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+    set_error("kernel_occupancy: no current device");
+    return KNND_ECUDA;
+  }
+  std::lock_guard<std::mutex> lock(g_occ_mu);
+  const OccKey key{dev, block, kern, smem};
+  auto it = g_occ.find(key);
+  if (it != g_occ.end()) {
+    *per_sm = it->second;
+    return KNND_OK;
+  }
+  size_t &lim = g_smem_attr[dev][kern];
+  if (smem > lim) {
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) {
+      set_error("cudaFuncSetAttribute(smem=%zu) failed: %s", smem, cudaGetErrorString(e));
+      return KNND_ECUDA;
+    }
+    lim = smem;
+  }
+  int n = 0;
+  const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, block, smem);
+  if (e != cudaSuccess) {
+    set_error("occupancy query failed: %s", cudaGetErrorString(e));
+    return KNND_ECUDA;
+  }
+  g_occ.emplace(key, n);
+  *per_sm = n;
+  return KNND_OK;
+}
 
 int num_sms() {
   int dev = 0, sms = 148;

@@ -17,6 +17,11 @@ constexpr unsigned FULL = 0xffffffffu;
 void set_error(const char *fmt, ...);
 void count_launch(unsigned n = 1);
 int num_sms();
+// blocks of `kern` resident per SM at (block threads, dynamic smem) on the current
+// device, raising the kernel's dynamic-smem limit to `smem` when needed; memoised
+// per (device, kernel, block, smem), so a round's launches make no attribute or
+// occupancy API calls after the first time (abi.cu).  Returns a KNND_* status.
+int kernel_occupancy(const void *kern, int block, size_t smem, int *per_sm);
 
 #define KNND_CHECK_ARG(cond, ...)            \
   do {                                       \

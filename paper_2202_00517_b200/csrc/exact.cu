@@ -544,7 +544,12 @@ static int launch_tc_screen(TcParams &p, const float *cand32, unsigned char *ima
   const size_t smem = L.total + 1024;
   const unsigned grid = (unsigned)((p.nq + TC_Q - 1) / TC_Q);
   auto launch = [&](auto kern) -> int {
-    KNND_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    if (int rc = kernel_occupancy((const void *)kern, TC_THREADS, smem, &per_sm)) return rc;
+    if (per_sm < 1) {
+      set_error("exact knn: the tensor-core screen cannot be resident (smem=%zu)", smem);
+      return KNND_EUNSUPPORTED;
+    }
     kern<<<grid, TC_THREADS, smem, st>>>(p);
     KNND_LAUNCHED(1);
     return KNND_OK;

@@ -1688,9 +1688,8 @@ static int launch_join(const JoinParams &p, const int32_t *alist, const int32_t 
     set_error("local join: shared memory %zu exceeds 227 KB (d=%d, H=%d)", smem, p.d, 1 << logH);
     return KNND_EUNSUPPORTED;
   }
-  KNND_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  KNND_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G, smem));
+  if (int rc = kernel_occupancy((const void *)kern, G, smem, &per_sm)) return rc;
   if (per_sm < 1) {
     set_error("local join: kernel cannot be resident (smem=%zu)", smem);
     return KNND_EUNSUPPORTED;
@@ -1715,9 +1714,8 @@ static int launch_warp(const JoinParams &p, const int32_t *alist, const int32_t 
   for (int wpb = WARP_BLOCK / 32; wpb >= 1; wpb >>= 1) {
     const size_t sm_b = L.total * wpb;
     if (sm_b > 227 * 1024) continue;
-    KNND_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_b));
     int per_sm = 0;
-    KNND_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpb * 32, sm_b));
+    if (int rc = kernel_occupancy((const void *)kern, wpb * 32, sm_b, &per_sm)) return rc;
     if (per_sm * wpb > best_warps) {
       best_warps = per_sm * wpb;
       best_wpb = wpb;
@@ -1728,7 +1726,6 @@ static int launch_warp(const JoinParams &p, const int32_t *alist, const int32_t 
     set_error("local join: warp slabs %zu B exceed 227 KB (d=%d, H=%d)", L.total, p.d, 1 << logH);
     return KNND_EUNSUPPORTED;
   }
-  KNND_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<(best_warps / best_wpb) * num_sms(), best_wpb * 32, smem, st>>>(p, alist, acount, logH, SW);
   KNND_LAUNCHED(1);
   return KNND_OK;

@@ -359,7 +359,8 @@ static int sort_rows_impl(const char *who, const double *pts, int pstride, const
   const int staged = (k <= 32 && staged_smem <= 160 * 1024) ? 1 : 0;
   size_t smem = staged ? staged_smem : (size_t)wpb * d * sizeof(double);
   if (k <= 32) {
-    KNND_CUDA(cudaFuncSetAttribute(sort_rows_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    if (int rc = kernel_occupancy((const void *)sort_rows_kernel<1>, 256, smem, &per_sm)) return rc;
     sort_rows_kernel<1><<<(unsigned)blocks, threads, smem, as_stream(stream)>>>(
         pts, pstride, log64, d64, xlogx, d, metric, k, row_lo, row_hi, draws, out_ids, out_kl, staged);
   } else {
