@@ -40,6 +40,13 @@ def test_invalid_config_exits_2(capsys, caplog):
     assert code == 2 and out == "" and "need n > k >= 2" in caplog.text
 
 
+def test_k_above_the_device_limit_exits_2(capsys, caplog):
+    """K > 64 (the device join's limit; the reference has none) is a ConfigError
+    with the reference CLI's exit code, raised before any device work."""
+    code, out, err = run_cli(capsys, "run", "--n", "1000", "--dim", "5", "--k", "100")
+    assert code == 2 and out == "" and "k must be <= 64" in caplog.text
+
+
 def test_missing_size_flags_exit_2(capsys):
     assert run_cli(capsys, "run", "--k", "4")[0] == 2
     assert run_cli(capsys, "sweep", "--k", "4", "--dims", "3")[0] == 2
