@@ -1636,6 +1636,19 @@ static Plan make_plan(int64_t n_items, int64_t m, int d, int K, int max_indeg) {
     c.logH = logH[i];
     c.lim = ((int64_t)1 << c.logH) / 2;
     c.sw = (int)(c.lim / K1 + 1);
+    // a shared-memory class must fit: the staged S list (up to lim / (K + 1)
+    // ids, double-buffered) grows as K shrinks (K = 2: a third of the table);
+    // the classes from the first that does not fit on are left to the
+    // global-memory class, whose S and table live in its slab
+    const size_t need = c.kind == KIND_WARP
+                            ? warp_slab(d, ld, 1 << c.logH, c.sw).total
+                            : smem_layout(c.kind == KIND_BLOCK128 ? 128 : c.kind == KIND_BLOCK256 ? 256 : 512, false,
+                                          d, ld, 1 << c.logH, c.sw)
+                                  .total;
+    if (i > 0 && need > 227 * 1024) {
+      n = i;
+      break;
+    }
     c.need = i == 0 || Pmax > prev;
     prev = c.lim;
   }
