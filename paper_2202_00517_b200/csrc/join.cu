@@ -39,6 +39,10 @@
 namespace knnd {
 
 constexpr int EMPTY = -1;
+// the screen's row format (template parameter SCR of the join kernels)
+constexpr int SCR_F32 = 0;  // fp32 log rows
+constexpr int SCR_Q15 = 1;  // 15-bit fixed point, fp32 second tier (knnd_kl_q15_prepare)
+constexpr int SCR_Q23 = 2;  // 23-bit fixed point in 3 bytes per entry (knnd_kl_q23_prepare)
 constexpr int UNR1 = 4;  // pre-dedup ids loaded per thread before inserting
 
 struct JoinParams {
@@ -58,8 +62,9 @@ struct JoinParams {
   int d, ld, K;
   float band;
   int nonpos;  // every log coordinate <= 0: sum |x log y| == -sum x log y exactly
-  const float *__restrict__ qh;  // Q15 screen: per-column steps h_j (log32 then points at the q15 rows)
-  int nvq;                       // Q15: 16-byte chunks per q15 row
+  const float *__restrict__ qh;  // Q15 / Q23 screen: per-column steps h_j (log32 then points at the quantised rows)
+  int nvq;                       // Q15 / Q23: 16-byte chunks per quantised row
+  int scr;                       // the screen's row format: SCR_F32 / SCR_Q15 / SCR_Q23
   const float *__restrict__ l32;  // Q15: the fp32 log rows (the second screening tier of R)
   const float *__restrict__ bound_in;  // per own row: max screened value of the current row (or NaN)
   float *__restrict__ bound_out;       // the same for the row written this round
@@ -190,16 +195,16 @@ __device__ __forceinline__ void stage_rows_f32(float *stage, const float *__rest
 
 // same, with the row ids held in registers: lane r holds ids of row r of the
 // batch (nrow <= 32), rows are fetched with a shuffle
-template <int NV4>
+template <int NV4, int SLD = NV4 * 4>
 __device__ __forceinline__ void stage_rows_f32_reg(float *stage, const float *__restrict__ log32, int idreg,
                                                    int nrow, int lane) {
-  constexpr int ld = NV4 * 4;
+  constexpr int ld = NV4 * 4;  // source row (floats); SLD: staged row stride
   constexpr int rpi = 32 / NV4;
   const int r0 = lane / NV4, part = lane - r0 * NV4;
-  unsigned dst = smem_u32(stage) + (unsigned)(r0 * ld + part * 4) * 4u;
+  unsigned dst = smem_u32(stage) + (unsigned)(r0 * SLD + part * 4) * 4u;
   const float *src = log32 + part * 4;
   const int iters = (nrow + rpi - 1) / rpi;
-  for (int t = 0; t < iters; ++t, dst += rpi * ld * 4u) {
+  for (int t = 0; t < iters; ++t, dst += rpi * SLD * 4u) {
     const int r = r0 + t * rpi;
     const int y = __shfl_sync(FULL, idreg, r & 31);
     if (r0 < rpi && r < nrow)
@@ -210,14 +215,14 @@ __device__ __forceinline__ void stage_rows_f32_reg(float *stage, const float *__
 // the warp kernel's variant of stage_rows_f32_reg: every lane executes every
 // shuffle, the copies are predicated, fixed unrolled iterations (the block
 // kernels measured slower with it)
-template <int NV4>
+template <int NV4, int SLD = NV4 * 4>
 __device__ __forceinline__ void stage_rows_f32_reg_full(float *stage, const float *__restrict__ log32, int idreg,
                                                         int nrow, int lane) {
-  constexpr int ld = NV4 * 4;
+  constexpr int ld = NV4 * 4;  // source row (floats); SLD: staged row stride
   constexpr int rpi = 32 / NV4;
   constexpr int ITERS = (32 + rpi - 1) / rpi;  // nrow <= 32: a fixed, fully unrolled count
   const int r0 = lane / NV4, part = lane - r0 * NV4;
-  const unsigned dst = smem_u32(stage) + (unsigned)(r0 * ld + part * 4) * 4u;
+  const unsigned dst = smem_u32(stage) + (unsigned)(r0 * SLD + part * 4) * 4u;
   const float *src = log32 + part * 4;
   const bool lane_on = r0 < rpi;
 #pragma unroll
@@ -225,7 +230,7 @@ __device__ __forceinline__ void stage_rows_f32_reg_full(float *stage, const floa
     const int r = r0 + t * rpi;
     const int y = __shfl_sync(FULL, idreg, r & 31);
     if (t * rpi < nrow && lane_on && r < nrow)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + (unsigned)(t * rpi * ld * 4)),
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + (unsigned)(t * rpi * SLD * 4)),
                    "l"(src + (int64_t)y * ld)
                    : "memory");
   }
@@ -357,6 +362,66 @@ __device__ __forceinline__ float screen_row_q15(const float *row, const float (&
     a3 = fmaf(w[8 * q + 7], __uint_as_float(__byte_perm(u.w, 0x3F000000u, 0x7324)), a3);
   }
   return -((a0 + a1) + (a2 + a3));
+}
+
+// ---------------------------------------------------------------------------
+// The 23-bit fixed-point screen (Q23: rows of 3 bytes per entry, 16 * NCH bytes
+// per row — 64 B at d = 20 instead of 80: two aligned sectors and one 128-B
+// line per row instead of three sectors over 1.5 lines; the random row gather
+// sets the join's rate, tools/row_probe.cu).  knnd_kl_q23_prepare stores, per
+// column j, q = round((Lmax_j - log y_j) / h_j) < 2^23, h_j = range_j / (2^23 - 1),
+// little endian.  One byte permute per entry builds the float whose bit
+// pattern is q (top byte 0 by replicating the sign of q's high byte, which is
+// 0): the denormal F_j = q_j 2^-149.  With w_j = x_j h_j 2^126 the screened
+// value v = sum_j w_j F_j = 2^-23 sum_j x_j h_j q_j equals
+// 2^-23 (ce + sum_j x_j Lmax_j) up to
+//   quantisation            2^-23 A1 / 2,  A1 = sum_j x_j h_j   (|q - exact| <= 1/2)
+//   fp32 weights and FMAs   (NQ + 12) 2^-24 v                    (every term >= 0: x_j > 0)
+// — the fp32 screen's error model (relative band on max v, plus an absolute
+// slack), so the threshold / certification rules are shared with it and the
+// fp64 ranking is the only second tier.
+template <int NCH>
+struct Q23 {
+  static constexpr int NQ = (16 * NCH) / 3;  // entries a row of NCH chunks holds
+};
+
+// the anchor's weights; returns the absolute (quantisation) part of its error bound
+template <int NCH>
+__device__ __forceinline__ float q23_weights(const double *x64, const float *__restrict__ qh, int d,
+                                             float (&w)[Q23<NCH>::NQ]) {
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < Q23<NCH>::NQ; ++j) {
+    const float x = j < d ? (float)x64[j] : 0.f;
+    const float h = j < d ? __ldg(qh + j) : 0.f;
+    w[j] = (x * h) * 0x1p126f;
+    s = fmaf(fabsf(w[j]), 0x1p-75f, s);
+  }
+  return s * 0x1p-75f * (1.f + 0x1p-9f) + 1e-36f;  // sum_j w_j 2^-150 = 2^-23 A1 / 2
+}
+
+template <int NCH>
+__device__ __forceinline__ float screen_row_q23(const float *row, const float (&w)[Q23<NCH>::NQ]) {
+  const uint4 *r4 = reinterpret_cast<const uint4 *>(row);
+  unsigned W[4 * NCH];
+#pragma unroll
+  for (int q = 0; q < NCH; ++q) {
+    const uint4 u = r4[q];
+    W[4 * q + 0] = u.x;
+    W[4 * q + 1] = u.y;
+    W[4 * q + 2] = u.z;
+    W[4 * q + 3] = u.w;
+  }
+  float a[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int j = 0; j < Q23<NCH>::NQ; ++j) {
+    const int k = (3 * j) >> 2, o = (3 * j) & 3;
+    const unsigned sel = o == 0 ? 0xA210u : o == 1 ? 0xB321u : o == 2 ? 0xC432u : 0xD543u;
+    unsigned bits;  // (prmt's sign-replication selector bit is outside __byte_perm's documented range)
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(bits) : "r"(W[k]), "r"(W[k + 1 < 4 * NCH ? k + 1 : k]), "r"(sel));
+    a[j & 3] = fmaf(w[j], __uint_as_float(bits), a[j & 3]);
+  }
+  return (a[0] + a[1]) + (a[2] + a[3]);
 }
 
 // issue cp.async copies of the fp64 log rows of ids[0..nrow) into stage
@@ -613,11 +678,12 @@ __device__ __forceinline__ void hist_find(const int *hist, int target, int *hdr,
   }
 }
 
-template <int G, int NV4, int KPL, bool GTAB, bool PF, bool Q15>
+template <int G, int NV4, int KPL, bool GTAB, bool PF, int SCR>
 __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__restrict__ alist,
                                                  const int32_t *__restrict__ acount, int logH, int SW,
                                                  int32_t *__restrict__ gslab, int64_t slab_ints) {
   constexpr int W = G / 32;
+  constexpr bool Q15 = SCR == SCR_Q15, Q23S = SCR == SCR_Q23, QX = SCR != SCR_F32;
   extern __shared__ __align__(16) unsigned char sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int H = 1 << logH;
@@ -637,7 +703,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     slabS = slab;
     table = slab + SW;
     list = table + H;
-    wrows = min(32, lstage_floats(p.ld) / (2 * (Q15 ? NV4 * 4 : p.ld)));  // rows per buffer, two buffers per warp
+    wrows = min(32, lstage_floats(p.ld) / (2 * (QX ? (Q23S ? (NV4 | 1) * 4 : NV4 * 4) : p.ld)));  // rows per buffer, two buffers per warp
     wstage = reinterpret_cast<float *>(sm + L.stage) + (size_t)warp * lstage_floats(p.ld);
     stage64 = reinterpret_cast<double *>(sm + L.stage);
     rcap64 = 32;
@@ -651,7 +717,11 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
   }
   const int K = p.K, K1 = K + 1;
   const int d = p.d;
-  const int ld = Q15 ? NV4 * 4 : p.ld;  // staged row stride (floats): the q15 rows are 16 * NV4 bytes
+  // staged row stride (floats): the quantised rows are 16 * NV4 bytes; Q23 rows are
+  // staged an odd number of 16-byte units apart (64-byte rows 64 bytes apart would
+  // make the screen's LDS.128 reads 4-way bank conflicts)
+  constexpr int SLD = Q23S ? (NV4 | 1) * 4 : NV4 * 4;
+  const int ld = QX ? SLD : p.ld;
   const int Gq = G / K1, Gr = G % K1;
   const int s_init = tid / K1, j_init = tid % K1;
   unsigned long long acc_comp = 0, acc_changed = 0, acc_bad = 0, acc_exact = 0;
@@ -876,13 +946,15 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
                              2 * wrows * ld <= per_warp_floats));
     }
     float mn = __int_as_float(0x7f800000), mx = -mn, am = 0.f;
-    const float slack = p.slack;
+    float slack = p.slack;
     float best0 = mn, best1 = mn;  // this lane's two smallest screened values
-    float4 xreg[NV4 > 0 && !Q15 ? NV4 : 1];  // the anchor's fp32 row in registers
-    float wq[Q15 ? 8 * NV4 : 1];               // Q15: the anchor's weights
+    float4 xreg[NV4 > 0 && !QX ? NV4 : 1];  // the anchor's fp32 row in registers
+    float wq[Q15 ? 8 * NV4 : Q23S ? Q23<Q23S ? NV4 : 1>::NQ : 1];  // Q15 / Q23: the anchor's weights
     float eb = 0.f;                             // Q15: the per-anchor screen error bound
     if constexpr (Q15) {
       eb = q15_weights<NV4>(x64, p.qh, d, wq);
+    } else if constexpr (Q23S) {
+      slack = q23_weights<NV4>(x64, p.qh, d, wq);  // the quantisation part of the bound, per anchor
     } else if constexpr (NV4 > 0) {
 #pragma unroll
       for (int q = 0; q < NV4; ++q) xreg[q] = reinterpret_cast<const float4 *>(x32)[q];
@@ -896,7 +968,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
       int id_after = (k0 + kstep < U && lane < wrows && k0 + kstep + lane < U) ? list[k0 + kstep + lane] : 0;
       if (k0 < U) {
         if constexpr (NV4 > 0)
-          stage_rows_f32_reg<NV4>(wstage, p.log32, id_next, min(wrows, U - k0), lane);
+          stage_rows_f32_reg<NV4, SLD>(wstage, p.log32, id_next, min(wrows, U - k0), lane);
         else
           stage_rows_f32<NV4>(wstage, p.log32, list + k0, min(wrows, U - k0), ld, lane);
         cp_async_commit();
@@ -906,7 +978,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
         const int k1 = k0 + kstep;
         if (k1 < U) {  // prefetch this warp's next batch into the other buffer
           if constexpr (NV4 > 0)
-            stage_rows_f32_reg<NV4>(wstage + (buf ^ 1) * wrows * ld, p.log32, id_after, min(wrows, U - k1), lane);
+            stage_rows_f32_reg<NV4, SLD>(wstage + (buf ^ 1) * wrows * ld, p.log32, id_after, min(wrows, U - k1), lane);
           else
             stage_rows_f32<NV4>(wstage + (buf ^ 1) * wrows * ld, p.log32, list + k1, min(wrows, U - k1), ld, lane);
           cp_async_commit();
@@ -924,6 +996,9 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
         if constexpr (Q15) {
           ce = screen_row_q15<NV4>(wstage + buf * wrows * ld + rl * ld, wq);
           ab = 0.f;
+        } else if constexpr (Q23S) {
+          ce = screen_row_q23<NV4>(wstage + buf * wrows * ld + rl * ld, wq);
+          ab = ce;  // every term is >= 0
         } else if constexpr (NV4 > 0) {
           screen_row_reg<NV4>(wstage + buf * wrows * ld + rl * ld, xreg, p.nonpos, ce, ab);
         } else {
@@ -1140,11 +1215,12 @@ __device__ __forceinline__ void prefetch_anchor(const JoinParams &p, int x, int6
   cp_async_commit();
 }
 
-template <int NV4, int KPL, bool VF, bool Q15>
+template <int NV4, int KPL, bool VF, int SCR>
 __global__ void __launch_bounds__(128, 4)
     join_warp_kernel(JoinParams p, const int32_t *__restrict__ alist, const int32_t *__restrict__ acount, int logH,
                      int SW) {
   constexpr int Q = 2 * KPL;  // per-lane kept screened values
+  constexpr bool Q15 = SCR == SCR_Q15, Q23S = SCR == SCR_Q23, QX = SCR != SCR_F32;
   extern __shared__ __align__(16) unsigned char sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int H = 1 << logH;
@@ -1164,7 +1240,11 @@ __global__ void __launch_bounds__(128, 4)
   double *stage64 = reinterpret_cast<double *>(table);         // phase 4: whole table
   const int K = p.K, K1 = K + 1;
   const int d = p.d, sd = p.d64 | 1;
-  const int ld = Q15 ? NV4 * 4 : p.ld;  // staged row stride (floats): the q15 rows are 16 * NV4 bytes
+  // staged row stride (floats): the quantised rows are 16 * NV4 bytes; Q23 rows are
+  // staged an odd number of 16-byte units apart (64-byte rows 64 bytes apart would
+  // make the screen's LDS.128 reads 4-way bank conflicts)
+  constexpr int SLD = Q23S ? (NV4 | 1) * 4 : NV4 * 4;
+  const int ld = QX ? SLD : p.ld;
   const int rcap64 = min(32, (4 * H) / (sd * 8));
   const int Gq = 32 / K1, Gr = 32 % K1;
   const int s_init = lane / K1, j_init = lane % K1;
@@ -1223,11 +1303,14 @@ __global__ void __launch_bounds__(128, 4)
     if (!p.aside32)
       for (int i = lane; i < p.ld; i += 32) x32[i] = i < d ? (float)x64[i] : 0.f;
     __syncwarp();
-    float4 xreg[NV4 > 0 && !Q15 ? NV4 : 1];  // the anchor's fp32 row in registers
-    float wq[Q15 ? 8 * NV4 : 1];               // Q15: the anchor's weights
+    float4 xreg[NV4 > 0 && !QX ? NV4 : 1];  // the anchor's fp32 row in registers
+    float wq[Q15 ? 8 * NV4 : Q23S ? Q23<Q23S ? NV4 : 1>::NQ : 1];  // Q15 / Q23: the anchor's weights
     float eb = 0.f;                             // Q15: the per-anchor screen error bound
+    float slack = p.slack;                      // the absolute part of the fp32 / Q23 bound
     if constexpr (Q15) {
       eb = q15_weights<NV4>(x64, p.qh, d, wq);
+    } else if constexpr (Q23S) {
+      slack = q23_weights<NV4>(x64, p.qh, d, wq);  // the quantisation part of the bound, per anchor
     } else if constexpr (NV4 > 0) {
 #pragma unroll
       for (int q = 0; q < NV4; ++q) xreg[q] = reinterpret_cast<const float4 *>(x32)[q];
@@ -1349,7 +1432,6 @@ __global__ void __launch_bounds__(128, 4)
 #pragma unroll
     for (int q = 0; q < Q; ++q) best[q] = __int_as_float(0x7f800000);
     float am = 0.f;
-    const float slack = p.slack;
     // ids of batch b+1 are in a register while batch b computes; batch b+2's are being loaded
     // two staging buffers in the table past the scores ([0, U), U <= H/2)
     const int u4 = (U + 3) & ~3;
@@ -1360,7 +1442,7 @@ __global__ void __launch_bounds__(128, 4)
     int id_after = (rows + lane < U && lane < rows) ? list[rows + lane] : 0;
     if (U > 0) {
       if constexpr (NV4 > 0)
-        stage_rows_f32_reg_full<NV4>(stage, p.log32, id_next, min(rows, U), lane);
+        stage_rows_f32_reg_full<NV4, SLD>(stage, p.log32, id_next, min(rows, U), lane);
       else
         stage_rows_f32<NV4>(stage, p.log32, list, min(rows, U), ld, lane);
       cp_async_commit();
@@ -1370,7 +1452,7 @@ __global__ void __launch_bounds__(128, 4)
       if (k0 + rows < U) {  // prefetch the next batch into the other buffer
         const int n1 = min(rows, U - k0 - rows);
         if constexpr (NV4 > 0)
-          stage_rows_f32_reg_full<NV4>(stage + (buf ^ 1) * rows * ld, p.log32, id_after, n1, lane);
+          stage_rows_f32_reg_full<NV4, SLD>(stage + (buf ^ 1) * rows * ld, p.log32, id_after, n1, lane);
         else
           stage_rows_f32<NV4>(stage + (buf ^ 1) * rows * ld, p.log32, list + k0 + rows, n1, ld, lane);
         cp_async_commit();
@@ -1392,6 +1474,9 @@ __global__ void __launch_bounds__(128, 4)
         if constexpr (Q15) {
           ce = screen_row_q15<NV4>(stage + buf * rows * ld + rl * ld, wq);
           ab = 0.f;
+        } else if constexpr (Q23S) {
+          ce = screen_row_q23<NV4>(stage + buf * rows * ld + rl * ld, wq);
+          ab = ce;  // every term is >= 0
         } else if constexpr (NV4 > 0) {
           screen_row_reg<NV4>(stage + buf * rows * ld + rl * ld, xreg, p.nonpos, ce, ab);
         } else {
@@ -1688,13 +1773,13 @@ static Plan make_plan(int64_t n_items, int64_t m, int d, int K, int max_indeg) {
   return P;
 }
 
-template <int G, int NV4, int KPL, bool GTAB, bool Q15 = false>
+template <int G, int NV4, int KPL, bool GTAB, int SCR = SCR_F32>
 static int launch_join(const JoinParams &p, const int32_t *alist, const int32_t *acount, int logH, int SW,
                        int32_t *gslab, int64_t slab_ints, int grid_cap, cudaStream_t st) {
   // friend ids two groups ahead pays for the larger shared tables (B128 at 2^13:
   // -8%); at 2^12 (at most 4 groups per anchor) it measured 20% slower
-  auto kern = (!GTAB && logH >= 13) ? join_kernel<G, NV4, KPL, GTAB, !GTAB, Q15>
-                                    : join_kernel<G, NV4, KPL, GTAB, false, Q15>;
+  auto kern = (!GTAB && logH >= 13) ? join_kernel<G, NV4, KPL, GTAB, !GTAB, SCR>
+                                    : join_kernel<G, NV4, KPL, GTAB, false, SCR>;
   const SmemLayout L = smem_layout(G, GTAB, p.d, p.ld, 1 << logH, SW);
   const size_t smem = L.total;
   if (smem > 227 * 1024) {
@@ -1714,11 +1799,11 @@ static int launch_join(const JoinParams &p, const int32_t *alist, const int32_t 
   return KNND_OK;
 }
 
-template <int NV4, int KPL, bool Q15 = false>
+template <int NV4, int KPL, int SCR = SCR_F32>
 static int launch_warp(const JoinParams &p, const int32_t *alist, const int32_t *acount, int logH, int SW,
                        cudaStream_t st) {
   // friend rows as int4 when they are 16-B aligned (K % 4 == 0)
-  auto kern = (p.K % 4 == 0) ? join_warp_kernel<NV4, KPL, true, Q15> : join_warp_kernel<NV4, KPL, false, Q15>;
+  auto kern = (p.K % 4 == 0) ? join_warp_kernel<NV4, KPL, true, SCR> : join_warp_kernel<NV4, KPL, false, SCR>;
   const WarpSlab L = warp_slab(p.d, p.ld, 1 << logH, SW);
   // warps per block: the largest of 4/2/1 that keeps the most warps resident
   // (big tables leave room for fewer than 4 slabs per block slot)
@@ -1757,9 +1842,17 @@ static int launch_warp(const JoinParams &p, const int32_t *alist, const int32_t 
 template <int G, bool GTAB>
 static int dispatch_block(const Plan &P, const JoinParams &p, const int32_t *alist, const int32_t *acount,
                           int logH, int SW, int32_t *gslab, int64_t slab_ints, int grid_cap, cudaStream_t st) {
-  if (p.qh) {  // the Q15 screen (K <= 32, rows of 2 or 3 16-byte chunks; checked at the entry)
-    if (p.nvq == 2) return launch_join<G, 2, 1, GTAB, true>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st);
-    return launch_join<G, 3, 1, GTAB, true>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st);
+  if (p.scr == SCR_Q15) {  // K <= 32, rows of 2 or 3 16-byte chunks; checked at the entry
+    if (p.nvq == 2)
+      return launch_join<G, 2, 1, GTAB, SCR_Q15>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st);
+    return launch_join<G, 3, 1, GTAB, SCR_Q15>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st);
+  }
+  if (p.scr == SCR_Q23) {  // K <= 32, rows of 2, 3 or 4 16-byte chunks; checked at the entry
+    if (p.nvq == 2)
+      return launch_join<G, 2, 1, GTAB, SCR_Q23>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st);
+    if (p.nvq == 3)
+      return launch_join<G, 3, 1, GTAB, SCR_Q23>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st);
+    return launch_join<G, 4, 1, GTAB, SCR_Q23>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st);
   }
 #define KNND_CALL(NV)                                                                                          \
   return P.kpl == 1 ? launch_join<G, NV, 1, GTAB>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st) \
@@ -1770,9 +1863,14 @@ static int dispatch_block(const Plan &P, const JoinParams &p, const int32_t *ali
 
 static int dispatch_warp(const Plan &P, const JoinParams &p, const int32_t *alist, const int32_t *acount, int logH,
                          int SW, cudaStream_t st) {
-  if (p.qh) {
-    if (p.nvq == 2) return launch_warp<2, 1, true>(p, alist, acount, logH, SW, st);
-    return launch_warp<3, 1, true>(p, alist, acount, logH, SW, st);
+  if (p.scr == SCR_Q15) {
+    if (p.nvq == 2) return launch_warp<2, 1, SCR_Q15>(p, alist, acount, logH, SW, st);
+    return launch_warp<3, 1, SCR_Q15>(p, alist, acount, logH, SW, st);
+  }
+  if (p.scr == SCR_Q23) {
+    if (p.nvq == 2) return launch_warp<2, 1, SCR_Q23>(p, alist, acount, logH, SW, st);
+    if (p.nvq == 3) return launch_warp<3, 1, SCR_Q23>(p, alist, acount, logH, SW, st);
+    return launch_warp<4, 1, SCR_Q23>(p, alist, acount, logH, SW, st);
   }
 #define KNND_CALL(NV)                                                             \
   return P.kpl == 1 ? launch_warp<NV, 1>(p, alist, acount, logH, SW, st) \
@@ -1854,6 +1952,7 @@ static int join_run(const char *who, JoinParams &p, int64_t n, int32_t dplan, in
   p.K = k;
   // rigorous bound on |fp32 screen - fp64| relative to sum |x*log y| (+ margin)
   p.band = (float)((ld32 + 8) * 0x1p-24);
+  if (p.scr == SCR_Q23) p.band = (float)(((16 * p.nvq) / 3 + 12) * 0x1p-24);  // NQ products, weights, chains
 
   KNND_CUDA(cudaMemsetAsync(counts, 0, 64, st));
   {
@@ -1975,7 +2074,7 @@ int knnd_local_join_peers(const double *points, const float *log32, const double
                           int32_t max_indeg, int32_t *out_ids, double *out_kl, int32_t *out_ucount,
                           unsigned long long *tally, const float *bound_in, float *bound_out, void *ws,
                           size_t ws_bytes, uint32_t flags, int32_t *const *peer_tables, int32_t npeers,
-                          const uint16_t *q15, const float *q15_h, int32_t ld16, void *stream, void *side_stream) {
+                          const void *qrows, const float *q_h, int32_t q_ld, void *stream, void *side_stream) {
   KNND_CHECK_ARG(points && log32 && log64 && xlogx, "knnd_local_join: null pointer");
   JoinParams p{};
   p.points = points;
@@ -1998,14 +2097,25 @@ int knnd_local_join_peers(const double *points, const float *log32, const double
   p.d64 = d;
   p.pstride = d;
   p.aside32 = nullptr;
-  if (q15) {  // the 15-bit fixed-point screen (knnd_kl_q15_prepare)
-    KNND_CHECK_ARG(q15_h && (ld16 == 16 || ld16 == 24) && ld16 >= d && k <= 32,
-                   "knnd_local_join: the q15 screen needs q15_h, ld16 16 or 24 (>= d) and K <= 32 (ld16=%d K=%d)",
-                   ld16, k);
+  if (qrows && (flags & KNND_JOIN_Q23)) {  // the 23-bit fixed-point screen (knnd_kl_q23_prepare)
+    KNND_CHECK_ARG(q_h && (q_ld == 32 || q_ld == 48 || q_ld == 64) && q_ld >= 3 * d && k <= 32,
+                   "knnd_local_join: the q23 screen needs q_h, rows of 32, 48 or 64 bytes (>= 3 d) and K <= 32 "
+                   "(q_ld=%d d=%d K=%d)",
+                   q_ld, d, k);
     p.l32 = log32;
-    p.log32 = reinterpret_cast<const float *>(q15);
-    p.qh = q15_h;
-    p.nvq = ld16 / 8;
+    p.log32 = reinterpret_cast<const float *>(qrows);
+    p.qh = q_h;
+    p.nvq = q_ld / 16;
+    p.scr = SCR_Q23;
+  } else if (qrows) {  // the 15-bit fixed-point screen (knnd_kl_q15_prepare)
+    KNND_CHECK_ARG(q_h && (q_ld == 16 || q_ld == 24) && q_ld >= d && k <= 32,
+                   "knnd_local_join: the q15 screen needs q_h, q_ld 16 or 24 (>= d) and K <= 32 (q_ld=%d K=%d)",
+                   q_ld, k);
+    p.l32 = log32;
+    p.log32 = reinterpret_cast<const float *>(qrows);
+    p.qh = q_h;
+    p.nvq = q_ld / 8;
+    p.scr = SCR_Q15;
   }
   if (int rc = set_peers(p, "knnd_local_join", peer_tables, npeers)) return rc;
   return join_run("knnd_local_join", p, n, d, k, row_lo, row_hi, max_indeg, ws, ws_bytes, stream, side_stream);

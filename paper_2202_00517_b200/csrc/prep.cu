@@ -86,6 +86,44 @@ __global__ void q15_quantize_kernel(const double *__restrict__ log64, int64_t n,
   }
 }
 
+// The 23-bit fixed-point log table of the join's Q23 screen (join.cu): per
+// column j, h_j = (max - min) / (2^23 - 1), q = round((max - log) / h_j),
+// 3 bytes per entry (little endian) at byte 3 j of a row of row_bytes bytes.
+// One thread per 4-byte word of the table; its bytes come from the (at most
+// two) entries that overlap it.
+__global__ void q23_quantize_kernel(const double *__restrict__ log64, int64_t n, int d, int row_bytes,
+                                    const unsigned long long *__restrict__ mm, uint32_t *__restrict__ q23,
+                                    float *__restrict__ qh) {
+  const int wpr = row_bytes >> 2;  // words per row
+  const int64_t total = n * wpr;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / wpr;
+    const int w = (int)(i - r * wpr);
+    uint32_t word = 0;
+    for (int j = (4 * w) / 3; 3 * j < 4 * w + 4; ++j) {  // entries overlapping bytes [4w, 4w+4)
+      if (j >= d) break;
+      const double lo = unord_f64(mm[j]), hi = unord_f64(mm[d + j]);
+      const double h = (hi - lo) / 8388607.0;
+      unsigned q = 0;
+      if (h > 0.0) {
+        double t = rint((hi - log64[r * d + j]) / h);
+        t = t < 0.0 ? 0.0 : (t > 8388607.0 ? 8388607.0 : t);
+        q = (unsigned)t;
+      }
+      const int sh = 8 * (3 * j - 4 * w);  // bit offset of the entry inside this word (may be negative)
+      word |= sh >= 0 ? (q << sh) : (q >> (-sh));
+    }
+    q23[i] = word;
+    if (r == 0) {
+      for (int j = w; j < row_bytes / 3; j += wpr) {  // row 0's threads also write qh
+        float hv = 0.f;
+        if (j < d) hv = (float)((unord_f64(mm[d + j]) - unord_f64(mm[j])) / 8388607.0);
+        qh[j] = hv;
+      }
+    }
+  }
+}
+
 // core.py:97-103 / similarity.py:101-106 — exact scores of ids against anchor x
 // (L2: similarity.py:135-140, pts = log64 = the vector rows with |v|^2 appended)
 __global__ void batch_scores_kernel(const double *__restrict__ pts, int pstride, const double *__restrict__ log64,
@@ -295,6 +333,31 @@ int knnd_kl_q15_prepare(const double *log64, int64_t n, int32_t d, int32_t ld16,
   int64_t blocks = (n * ld16 + 255) / 256;
   if (blocks > (int64_t)num_sms() * 32) blocks = (int64_t)num_sms() * 32;
   q15_quantize_kernel<<<(unsigned)blocks, 256, 0, st>>>(log64, n, d, ld16, mm, q15, qh);
+  KNND_LAUNCHED(1);
+  return KNND_OK;
+}
+
+int knnd_kl_q23_prepare(const double *log64, int64_t n, int32_t d, int32_t row_bytes, uint8_t *q23, float *qh,
+                        void *ws, size_t ws_bytes, void *stream) {
+  KNND_CHECK_ARG(log64 && q23 && qh, "knnd_kl_q23_prepare: null pointer");
+  KNND_CHECK_ARG(n >= 1 && d >= 1 && d <= 256, "knnd_kl_q23_prepare: bad shape n=%lld d=%d", (long long)n, d);
+  KNND_CHECK_ARG(row_bytes >= 3 * d && row_bytes % 16 == 0,
+                 "knnd_kl_q23_prepare: row_bytes=%d must be >= 3 d and a multiple of 16", row_bytes);
+  if (!ws || ws_bytes < knnd_kl_q15_workspace_bytes(d)) {
+    set_error("knnd_kl_q23_prepare: workspace %zu < %zu bytes", ws_bytes, knnd_kl_q15_workspace_bytes(d));
+    return KNND_EWORKSPACE;
+  }
+  cudaStream_t st = as_stream(stream);
+  unsigned long long *mm = static_cast<unsigned long long *>(ws);
+  KNND_CUDA(cudaMemsetAsync(mm, 0xFF, (size_t)d * 8, st));
+  KNND_CUDA(cudaMemsetAsync(mm + d, 0x00, (size_t)d * 8, st));
+  const int threads = (256 / d) * d > 0 ? (256 / d) * d : d;
+  col_minmax_kernel<<<num_sms() * 4, threads, 0, st>>>(log64, n, d, mm);
+  KNND_LAUNCHED(1);
+  int64_t blocks = (n * (row_bytes / 4) + 255) / 256;
+  if (blocks > (int64_t)num_sms() * 32) blocks = (int64_t)num_sms() * 32;
+  q23_quantize_kernel<<<(unsigned)blocks, 256, 0, st>>>(log64, n, d, row_bytes, mm,
+                                                        reinterpret_cast<uint32_t *>(q23), qh);
   KNND_LAUNCHED(1);
   return KNND_OK;
 }

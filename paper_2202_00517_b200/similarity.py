@@ -145,9 +145,25 @@ class DeviceTables:
         # than 80-byte ones; results do not depend on it (KNND_Q15=0/1 forces it)
         self.q15 = self.qh = None
         self.ld16 = (self.d + 7) // 8 * 8
+        # the join's 23-bit screen (knnd_kl_q23_prepare): 3 bytes per entry, rows of
+        # 32 / 48 / 64 bytes (d <= 10 / 16 / 21) — at d = 20 two aligned sectors in
+        # one 128-B line per row instead of three sectors over 1.5 lines, with an
+        # error bound as tight as the fp32 screen's.  KNND_Q23=0/1 forces it off / on.
+        self.q23 = self.qh23 = None
+        self.q23_bytes = (3 * self.d + 15) // 16 * 16
+        force23 = os.environ.get("KNND_Q23")
+        if force23 == "1" and self.q23_bytes <= 64:
+            self.q23 = torch.empty((self.n, self.q23_bytes), dtype=torch.uint8, device=device)
+            self.qh23 = torch.empty(self.q23_bytes // 3, dtype=torch.float32, device=device)
+            ws = torch.empty(max(int(_lib.load().knnd_kl_q15_workspace_bytes(self.d)), 256), dtype=torch.uint8,
+                             device=device)
+            _lib.call("knnd_kl_q23_prepare", self.log64.data_ptr(), self.n, self.d, self.q23_bytes,
+                      self.q23.data_ptr(), self.qh23.data_ptr(), ws.data_ptr(), ws.numel(), _stream(device))
+            if not bool(torch.isfinite(self.qh23).all().item()):  # a non-finite log: keep the fp32 screen
+                self.q23 = self.qh23 = None
         force = os.environ.get("KNND_Q15")
         want = force == "1" or (force is None and self.n * self.ld * 4 > Q15_MIN_BYTES)
-        if want and self.ld16 in (16, 24):
+        if want and self.ld16 in (16, 24) and self.q23 is None:
             self.q15 = torch.empty((self.n, self.ld16), dtype=torch.int16, device=device)
             self.qh = torch.empty(self.ld16, dtype=torch.float32, device=device)
             ws = torch.empty(max(int(_lib.load().knnd_kl_q15_workspace_bytes(self.d)), 256), dtype=torch.uint8,
@@ -160,6 +176,14 @@ class DeviceTables:
     def join(self, table, k, csr, max_indeg, out_rows, tally, out_scores, out_ucount, bound_in, bound_out, ws,
              flags, stream, peers=(), side_stream=None):
         q15 = self.q15 is not None and k <= 32  # (the same choice every round of a descent: K is fixed)
+        if self.q23 is not None and k <= 32:
+            _lib.call("knnd_local_join_peers", self.points.data_ptr(), self.log32.data_ptr(), self.log64.data_ptr(),
+                      self.xlogx.data_ptr(), self.n, self.d, self.ld, table.data_ptr(), k, csr.indptr.data_ptr(),
+                      csr.indices.data_ptr(), csr.lo, csr.hi, max_indeg, out_rows.data_ptr(), _ptr(out_scores),
+                      _ptr(out_ucount), tally.data_ptr(), _ptr(bound_in), _ptr(bound_out), ws.data_ptr(), ws.numel(),
+                      flags | _lib.JOIN_Q23, _lib.peer_array(peers), len(peers), self.q23.data_ptr(),
+                      self.qh23.data_ptr(), self.q23_bytes, stream, side_stream)
+            return
         _lib.call("knnd_local_join_peers", self.points.data_ptr(), self.log32.data_ptr(), self.log64.data_ptr(),
                   self.xlogx.data_ptr(), self.n, self.d, self.ld, table.data_ptr(), k, csr.indptr.data_ptr(),
                   csr.indices.data_ptr(), csr.lo, csr.hi, max_indeg, out_rows.data_ptr(), _ptr(out_scores),
