@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define KNND_ABI_VERSION 2
+#define KNND_ABI_VERSION 3
 
 enum {
   KNND_OK = 0,
@@ -121,7 +121,6 @@ int knnd_csr_build(const int32_t *friends, int64_t n, int32_t k, int64_t row_lo,
  * Results do not depend on flags (only the work does).
  */
 #define KNND_JOIN_NONPOS_LOG 1u
-#define KNND_JOIN_Q23 2u /* knnd_local_join_peers: qrows holds knnd_kl_q23_prepare rows (else q15 rows) */
 #define KNND_MAX_PEERS 15
 size_t knnd_local_join_workspace_bytes(int64_t n, int32_t d, int32_t k, int64_t row_lo,
                                        int64_t row_hi, int32_t max_indeg);
@@ -145,14 +144,13 @@ int knnd_local_join(const double *points, const float *log32, const double *log6
  * memory over NVLink).  The stores overlap the join; before any rank reads the
  * gathered table, the caller runs a cross-rank barrier on the stream (the
  * kernels end with a system-scope fence).  npeers in 0..KNND_MAX_PEERS.
- * qrows / q_h / q_ld (nullable qrows): screen with a fixed-point copy of the
- * log table instead of log32 (K <= 32) — the random row gather sets the
- * join's rate, and smaller rows move faster.  With flags & KNND_JOIN_Q23 the
- * rows are knnd_kl_q23_prepare's (q_ld = 32, 48 or 64 bytes per row, >= 3 d:
- * 23 bits per entry, an error bound as tight as the fp32 screen's); otherwise
- * knnd_kl_q15_prepare's (q_ld = 16 or 24 entries per row, >= d: 15 bits per
- * entry, a wider bound and an fp32 second tier).  The fp64 decision is
- * unchanged, so results do not depend on the screen.
+ * qrows / q_h / q_ld (nullable qrows): screen with the 23-bit fixed-point copy
+ * of the log table (knnd_kl_q23_prepare: q_ld = 16, 32, 48 or 64 bytes per row,
+ * >= 3 d; K <= 32) instead of log32 — the random row gather sets the join's
+ * rate and smaller rows move faster (64-byte rows at d = 20: two aligned
+ * sectors in one 128-byte line, against three sectors over 1.5 lines); the
+ * error bound is as tight as the fp32 screen's and the fp64 decision is
+ * unchanged, so results do not depend on it.
  * side_stream (nullable, a stream of the same device other than `stream`):
  * the few long anchors of the big-table size classes run there, concurrently
  * with the bulk classes on `stream`; the call forks to it and joins back, so
@@ -171,18 +169,6 @@ int knnd_local_join_peers(const double *points, const float *log32, const double
                           void *side_stream);
 
 /*
- * The 15-bit fixed-point copy of the log table for the join's q15 screen:
- * per column j, L0_j = min log, h_j = (max log - L0_j) / 32767 (0 for a
- * constant column), q = round((log64 - L0_j) / h_j) in 0..32767, stored as
- * 0x8000 | q in rows of ld16 entries (ld16 % 8 == 0, >= d; padding 0x8000);
- * qh[j] = (float)h_j (ld16 floats, 0 past d).  |log - (L0_j + h_j q)| <= h_j / 2.
- * Workspace: knnd_kl_q15_workspace_bytes(d).
- */
-size_t knnd_kl_q15_workspace_bytes(int32_t d);
-int knnd_kl_q15_prepare(const double *log64, int64_t n, int32_t d, int32_t ld16, uint16_t *q15,
-                        float *qh, void *ws, size_t ws_bytes, void *stream);
-
-/*
  * The 23-bit fixed-point copy of the log table for the join's q23 screen:
  * per column j, h_j = (max log - min log) / (2^23 - 1) (0 for a constant
  * column), q = round((max log - log64) / h_j) in 0..2^23-1, stored in 3 bytes
@@ -190,8 +176,9 @@ int knnd_kl_q15_prepare(const double *log64, int64_t n, int32_t d, int32_t ld16,
  * >= 3 d; padding 0); qh[j] = (float)h_j (row_bytes / 3 floats, 0 past d).
  * |(max log - h_j q) - log| <= h_j / 2.  A table with a non-finite log yields
  * non-finite qh entries: the caller must then keep the fp32 screen.
- * Workspace: knnd_kl_q15_workspace_bytes(d).
+ * Workspace: knnd_kl_q23_workspace_bytes(d).
  */
+size_t knnd_kl_q23_workspace_bytes(int32_t d);
 int knnd_kl_q23_prepare(const double *log64, int64_t n, int32_t d, int32_t row_bytes, uint8_t *q23,
                         float *qh, void *ws, size_t ws_bytes, void *stream);
 

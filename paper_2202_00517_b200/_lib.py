@@ -40,8 +40,7 @@ _SIGS = {
                          _P, _P, _P, _SZ, C.c_uint32, _P], C.c_int),
     "knnd_local_join_peers": ([_P, _P, _P, _P, _I64, _I32, _I32, _P, _I32, _P, _P, _I64, _I64, _I32, _P, _P, _P,
                                _P, _P, _P, _P, _SZ, C.c_uint32, _P, _I32, _P, _P, _I32, _P, _P], C.c_int),
-    "knnd_kl_q15_workspace_bytes": ([_I32], _SZ),
-    "knnd_kl_q15_prepare": ([_P, _I64, _I32, _I32, _P, _P, _P, _SZ, _P], C.c_int),
+    "knnd_kl_q23_workspace_bytes": ([_I32], _SZ),
     "knnd_kl_q23_prepare": ([_P, _I64, _I32, _I32, _P, _P, _P, _SZ, _P], C.c_int),
     "knnd_fcc": ([_P, _I64, _I32, _P, _P, _P, _I32, _P, _P], C.c_int),
     "knnd_sort_rows": ([_P, _P, _P, _I64, _I32, _I32, _I64, _I64, _P, _P, _P, _P], C.c_int),
@@ -65,7 +64,6 @@ _SIGS = {
 EXPORTS = tuple(_SIGS)
 
 JOIN_NONPOS_LOG = 1  # KNND_JOIN_NONPOS_LOG
-JOIN_Q23 = 2  # KNND_JOIN_Q23
 MAX_PEERS = 15  # KNND_MAX_PEERS
 
 

@@ -41,8 +41,7 @@ namespace knnd {
 constexpr int EMPTY = -1;
 // the screen's row format (template parameter SCR of the join kernels)
 constexpr int SCR_F32 = 0;  // fp32 log rows
-constexpr int SCR_Q15 = 1;  // 15-bit fixed point, fp32 second tier (knnd_kl_q15_prepare)
-constexpr int SCR_Q23 = 2;  // 23-bit fixed point in 3 bytes per entry (knnd_kl_q23_prepare)
+constexpr int SCR_Q23 = 1;  // 23-bit fixed point in 3 bytes per entry (knnd_kl_q23_prepare)
 constexpr int UNR1 = 4;  // pre-dedup ids loaded per thread before inserting
 
 struct JoinParams {
@@ -62,10 +61,9 @@ struct JoinParams {
   int d, ld, K;
   float band;
   int nonpos;  // every log coordinate <= 0: sum |x log y| == -sum x log y exactly
-  const float *__restrict__ qh;  // Q15 / Q23 screen: per-column steps h_j (log32 then points at the quantised rows)
-  int nvq;                       // Q15 / Q23: 16-byte chunks per quantised row
-  int scr;                       // the screen's row format: SCR_F32 / SCR_Q15 / SCR_Q23
-  const float *__restrict__ l32;  // Q15: the fp32 log rows (the second screening tier of R)
+  const float *__restrict__ qh;  // Q23 screen: per-column steps h_j (log32 then points at the quantised rows)
+  int nvq;                       // Q23: 16-byte chunks per quantised row
+  int scr;                       // the screen's row format: SCR_F32 / SCR_Q23
   const float *__restrict__ bound_in;  // per own row: max screened value of the current row (or NaN)
   float *__restrict__ bound_out;       // the same for the row written this round
   // metric (score.cuh): KL, or squared Euclidean (EuclideanRankingSystem, similarity.py:119-140)
@@ -318,53 +316,6 @@ __device__ __forceinline__ void screen_row_reg(const float *row, const float4 (&
 }
 
 // ---------------------------------------------------------------------------
-// The 15-bit fixed-point screen (Q15: tables larger than L2, where the random
-// row gather runs at DRAM speed and the row's byte count sets the rate; rows
-// of 8*NV4 entries of 0x8000 | q, knnd_kl_q15_prepare).  With log y_j =
-// L0_j + h_j q_j + e_j (|e_j| <= h_j / 2) and F_j = 1 + q_j 2^-15 (built
-// exactly from the stored half-word by one byte permute), the screened value
-// v = -sum_j w_j F_j, w_j = x_j h_j 2^15, equals the cross entropy minus a
-// per-anchor constant (2^15 sum_j x_j h_j - sum_j x_j L0_j) minus sum_j x_j e_j.
-// The error bound per anchor: A1 = sum_j |x_j| h_j;
-//   quantisation            A1 / 2
-//   fp32 weights and FMAs   (8 NV4 + 4) 2^-23 * sum_j |w_j F_j| <= (8 NV4 + 4) 2^-23 * 2^16 A1
-// so eb = A1 (1/2 + (8 NV4 + 4) 2^-7), generously; screened values of one
-// anchor then obey |v - (ce - const)| <= eb, which takes the place of
-// band * am + slack in the threshold and certification rules.
-template <int NV4>
-__device__ __forceinline__ float q15_weights(const double *x64, const float *__restrict__ qh, int d,
-                                             float (&w)[8 * NV4]) {
-  float a1 = 0.f;
-#pragma unroll
-  for (int j = 0; j < 8 * NV4; ++j) {
-    const float x = j < d ? (float)x64[j] : 0.f;
-    const float h = j < d ? __ldg(qh + j) : 0.f;
-    w[j] = x * h * 32768.f;
-    a1 = fmaf(fabsf(x), h, a1);
-  }
-  return a1 * (1.f + 0x1p-16f) * (0.5f + (8 * NV4 + 4) * 0x1p-7f);
-}
-
-template <int NV4>
-__device__ __forceinline__ float screen_row_q15(const float *row, const float (&w)[8 * NV4]) {
-  const uint4 *r4 = reinterpret_cast<const uint4 *>(row);
-  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll
-  for (int q = 0; q < NV4; ++q) {
-    const uint4 u = r4[q];
-    a0 = fmaf(w[8 * q + 0], __uint_as_float(__byte_perm(u.x, 0x3F000000u, 0x7104)), a0);
-    a1 = fmaf(w[8 * q + 1], __uint_as_float(__byte_perm(u.x, 0x3F000000u, 0x7324)), a1);
-    a2 = fmaf(w[8 * q + 2], __uint_as_float(__byte_perm(u.y, 0x3F000000u, 0x7104)), a2);
-    a3 = fmaf(w[8 * q + 3], __uint_as_float(__byte_perm(u.y, 0x3F000000u, 0x7324)), a3);
-    a0 = fmaf(w[8 * q + 4], __uint_as_float(__byte_perm(u.z, 0x3F000000u, 0x7104)), a0);
-    a1 = fmaf(w[8 * q + 5], __uint_as_float(__byte_perm(u.z, 0x3F000000u, 0x7324)), a1);
-    a2 = fmaf(w[8 * q + 6], __uint_as_float(__byte_perm(u.w, 0x3F000000u, 0x7104)), a2);
-    a3 = fmaf(w[8 * q + 7], __uint_as_float(__byte_perm(u.w, 0x3F000000u, 0x7324)), a3);
-  }
-  return -((a0 + a1) + (a2 + a3));
-}
-
-// ---------------------------------------------------------------------------
 // The 23-bit fixed-point screen (Q23: rows of 3 bytes per entry, 16 * NCH bytes
 // per row — 64 B at d = 20 instead of 80: two aligned sectors and one 128-B
 // line per row instead of three sectors over 1.5 lines; the random row gather
@@ -547,29 +498,6 @@ __device__ __forceinline__ bool certify_row(const JoinParams &p, const int32_t *
   return true;
 }
 
-// The Q15 screen's second tier: when its (wider) bound cannot certify R's
-// order, rescreen the members of R (<= 32) with their fp32 log rows — the
-// fp32 bound of the local join, ~100x tighter — and certify that order; the
-// fp64 ranking runs only if this fails too.  `vals` (R's screened values) are
-// overwritten; the row bound stays theta (it must be in Q15 units).
-__device__ __forceinline__ bool certify_row_f32(const JoinParams &p, const int32_t *ids, float *vals, int nR,
-                                                float *stage, const float *x32, int x, int64_t xr, int lane,
-                                                bool &diff) {
-  const int ld = p.ld;  // the fp32 row length
-  stage_rows_f32<0>(stage, p.l32, ids, nR, ld, lane);
-  cp_async_wait_all();
-  __syncwarp();
-  float ce = __int_as_float(0x7f800000), ab = 0.f;
-  if (lane < nR) screen_row<0>(stage + lane * ld, x32, ld, p.nonpos, ce, ab);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) ab = fmaxf(ab, __shfl_xor_sync(FULL, ab, o));
-  __syncwarp();
-  if (lane < nR) vals[lane] = ce;
-  __syncwarp();
-  float kth_unused;
-  return certify_row(p, ids, vals, nR, 2.f * p.band * ab, x, xr, lane, diff, kth_unused);
-}
-
 // ---------------------------------------------------------------------------
 // block-per-anchor kernel (classes B and L)
 
@@ -683,7 +611,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
                                                  const int32_t *__restrict__ acount, int logH, int SW,
                                                  int32_t *__restrict__ gslab, int64_t slab_ints) {
   constexpr int W = G / 32;
-  constexpr bool Q15 = SCR == SCR_Q15, Q23S = SCR == SCR_Q23, QX = SCR != SCR_F32;
+  constexpr bool Q23S = SCR == SCR_Q23;
   extern __shared__ __align__(16) unsigned char sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int H = 1 << logH;
@@ -703,7 +631,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     slabS = slab;
     table = slab + SW;
     list = table + H;
-    wrows = min(32, lstage_floats(p.ld) / (2 * (QX ? (Q23S ? (NV4 | 1) * 4 : NV4 * 4) : p.ld)));  // rows per buffer, two buffers per warp
+    wrows = min(32, lstage_floats(p.ld) / (2 * (Q23S ? (NV4 | 1) * 4 : p.ld)));  // rows per buffer, two buffers per warp
     wstage = reinterpret_cast<float *>(sm + L.stage) + (size_t)warp * lstage_floats(p.ld);
     stage64 = reinterpret_cast<double *>(sm + L.stage);
     rcap64 = 32;
@@ -717,11 +645,11 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
   }
   const int K = p.K, K1 = K + 1;
   const int d = p.d;
-  // staged row stride (floats): the quantised rows are 16 * NV4 bytes; Q23 rows are
-  // staged an odd number of 16-byte units apart (64-byte rows 64 bytes apart would
-  // make the screen's LDS.128 reads 4-way bank conflicts)
+  // staged row stride (floats): the Q23 rows are 16 * NV4 bytes, staged an odd
+  // number of 16-byte units apart (64-byte rows 64 bytes apart would make the
+  // screen's LDS.128 reads 4-way bank conflicts)
   constexpr int SLD = Q23S ? (NV4 | 1) * 4 : NV4 * 4;
-  const int ld = QX ? SLD : p.ld;
+  const int ld = Q23S ? SLD : p.ld;
   const int Gq = G / K1, Gr = G % K1;
   const int s_init = tid / K1, j_init = tid % K1;
   unsigned long long acc_comp = 0, acc_changed = 0, acc_bad = 0, acc_exact = 0;
@@ -948,12 +876,9 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     float mn = __int_as_float(0x7f800000), mx = -mn, am = 0.f;
     float slack = p.slack;
     float best0 = mn, best1 = mn;  // this lane's two smallest screened values
-    float4 xreg[NV4 > 0 && !QX ? NV4 : 1];  // the anchor's fp32 row in registers
-    float wq[Q15 ? 8 * NV4 : Q23S ? Q23<Q23S ? NV4 : 1>::NQ : 1];  // Q15 / Q23: the anchor's weights
-    float eb = 0.f;                             // Q15: the per-anchor screen error bound
-    if constexpr (Q15) {
-      eb = q15_weights<NV4>(x64, p.qh, d, wq);
-    } else if constexpr (Q23S) {
+    float4 xreg[NV4 > 0 && !Q23S ? NV4 : 1];  // the anchor's fp32 row in registers
+    float wq[Q23<Q23S ? NV4 : 1>::NQ];  // Q23: the anchor's weights
+    if constexpr (Q23S) {
       slack = q23_weights<NV4>(x64, p.qh, d, wq);  // the quantisation part of the bound, per anchor
     } else if constexpr (NV4 > 0) {
 #pragma unroll
@@ -993,10 +918,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
         const bool in = rr < nrow;
         const int rl = in ? rr : 0;
         float ce, ab;
-        if constexpr (Q15) {
-          ce = screen_row_q15<NV4>(wstage + buf * wrows * ld + rl * ld, wq);
-          ab = 0.f;
-        } else if constexpr (Q23S) {
+        if constexpr (Q23S) {
           ce = screen_row_q23<NV4>(wstage + buf * wrows * ld + rl * ld, wq);
           ab = ce;  // every term is >= 0
         } else if constexpr (NV4 > 0) {
@@ -1039,7 +961,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
         float ab = 0.f;
 #pragma unroll
         for (int w = 0; w < W; ++w) ab = fmaxf(ab, red[w * 4 + 2]);
-        const float th0 = T0 + 2.f * (Q15 ? eb : p.band * ab + slack) + fabsf(T0) * 1e-6f;
+        const float th0 = T0 + 2.f * (p.band * ab + slack) + fabsf(T0) * 1e-6f;
         collect_r(scores, list, U, th0, R, rval, &hdr[1], tid, lane, G);
         __syncthreads();
         if (hdr[1] <= 32) {
@@ -1122,7 +1044,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
         T += (fabsf(T) + range) * 1e-6f;  // covers the rounding of t and of this line
       }
     }
-    const float ebase = Q15 ? eb : p.band * am + slack;  // the screen's error bound at this anchor
+    const float ebase = p.band * am + slack;  // the screen's error bound at this anchor
     const float theta = T + 2.f * ebase + fabsf(T) * 1e-6f;
     if (hdr[8] < count) prefetch(pb ^ 1, hdr[9], hdr64[0], hdr[12]);
 
@@ -1138,8 +1060,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
       bool diff;
       float kth = theta;  // every member of the new row has a screened value <= theta
       if (!(KPL == 1 && p.out_kl == nullptr && nR <= 32 &&
-            (certify_row(p, R, rval, nR, 2.f * ebase, x, xr, lane, diff, kth) ||
-             (Q15 && certify_row_f32(p, R, rval, nR, reinterpret_cast<float *>(stage64), x32, x, xr, lane, diff))))) {
+            certify_row(p, R, rval, nR, 2.f * ebase, x, xr, lane, diff, kth))) {
         diff = exact_row<KPL>(p, R, nR, stage64, rcap64, x64, x, xr, lane);
         ++acc_exact;
       }
@@ -1220,7 +1141,7 @@ __global__ void __launch_bounds__(128, 4)
     join_warp_kernel(JoinParams p, const int32_t *__restrict__ alist, const int32_t *__restrict__ acount, int logH,
                      int SW) {
   constexpr int Q = 2 * KPL;  // per-lane kept screened values
-  constexpr bool Q15 = SCR == SCR_Q15, Q23S = SCR == SCR_Q23, QX = SCR != SCR_F32;
+  constexpr bool Q23S = SCR == SCR_Q23;
   extern __shared__ __align__(16) unsigned char sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int H = 1 << logH;
@@ -1240,11 +1161,11 @@ __global__ void __launch_bounds__(128, 4)
   double *stage64 = reinterpret_cast<double *>(table);         // phase 4: whole table
   const int K = p.K, K1 = K + 1;
   const int d = p.d, sd = p.d64 | 1;
-  // staged row stride (floats): the quantised rows are 16 * NV4 bytes; Q23 rows are
-  // staged an odd number of 16-byte units apart (64-byte rows 64 bytes apart would
-  // make the screen's LDS.128 reads 4-way bank conflicts)
+  // staged row stride (floats): the Q23 rows are 16 * NV4 bytes, staged an odd
+  // number of 16-byte units apart (64-byte rows 64 bytes apart would make the
+  // screen's LDS.128 reads 4-way bank conflicts)
   constexpr int SLD = Q23S ? (NV4 | 1) * 4 : NV4 * 4;
-  const int ld = QX ? SLD : p.ld;
+  const int ld = Q23S ? SLD : p.ld;
   const int rcap64 = min(32, (4 * H) / (sd * 8));
   const int Gq = 32 / K1, Gr = 32 % K1;
   const int s_init = lane / K1, j_init = lane % K1;
@@ -1303,13 +1224,10 @@ __global__ void __launch_bounds__(128, 4)
     if (!p.aside32)
       for (int i = lane; i < p.ld; i += 32) x32[i] = i < d ? (float)x64[i] : 0.f;
     __syncwarp();
-    float4 xreg[NV4 > 0 && !QX ? NV4 : 1];  // the anchor's fp32 row in registers
-    float wq[Q15 ? 8 * NV4 : Q23S ? Q23<Q23S ? NV4 : 1>::NQ : 1];  // Q15 / Q23: the anchor's weights
-    float eb = 0.f;                             // Q15: the per-anchor screen error bound
+    float4 xreg[NV4 > 0 && !Q23S ? NV4 : 1];  // the anchor's fp32 row in registers
+    float wq[Q23<Q23S ? NV4 : 1>::NQ];  // Q23: the anchor's weights
     float slack = p.slack;                      // the absolute part of the fp32 / Q23 bound
-    if constexpr (Q15) {
-      eb = q15_weights<NV4>(x64, p.qh, d, wq);
-    } else if constexpr (Q23S) {
+    if constexpr (Q23S) {
       slack = q23_weights<NV4>(x64, p.qh, d, wq);  // the quantisation part of the bound, per anchor
     } else if constexpr (NV4 > 0) {
 #pragma unroll
@@ -1471,10 +1389,7 @@ __global__ void __launch_bounds__(128, 4)
         const bool in = rr < nrow;
         const int rl = in ? rr : 0;  // lanes past nrow recompute row 0, discarded
         float ce, ab;
-        if constexpr (Q15) {
-          ce = screen_row_q15<NV4>(stage + buf * rows * ld + rl * ld, wq);
-          ab = 0.f;
-        } else if constexpr (Q23S) {
+        if constexpr (Q23S) {
           ce = screen_row_q23<NV4>(stage + buf * rows * ld + rl * ld, wq);
           ab = ce;  // every term is >= 0
         } else if constexpr (NV4 > 0) {
@@ -1527,7 +1442,7 @@ __global__ void __launch_bounds__(128, 4)
       return t;
     };
     float T;
-    const float ebase = Q15 ? eb : p.band * am + slack;  // the screen's error bound at this anchor
+    const float ebase = p.band * am + slack;  // the screen's error bound at this anchor
     if (KPL == 1 && isfinite(T0)) {
       const float th0 = T0 + 2.f * ebase + fabsf(T0) * 1e-6f;
       int cnt = 0;
@@ -1562,8 +1477,7 @@ __global__ void __launch_bounds__(128, 4)
     bool diff;
     float kth = theta;  // every member of the new row has a screened value <= theta
     if (!(KPL == 1 && p.out_kl == nullptr && nR <= 32 &&
-          (certify_row(p, list, scores, nR, 2.f * ebase, x, xr, lane, diff, kth) ||
-           (Q15 && certify_row_f32(p, list, scores, nR, scores + 32, x32, x, xr, lane, diff))))) {
+          certify_row(p, list, scores, nR, 2.f * ebase, x, xr, lane, diff, kth))) {
       diff = exact_row<KPL>(p, list, nR, stage64, rcap64, x64, x, xr, lane);
       ++acc_exact;
     }
@@ -1842,12 +1756,9 @@ static int launch_warp(const JoinParams &p, const int32_t *alist, const int32_t 
 template <int G, bool GTAB>
 static int dispatch_block(const Plan &P, const JoinParams &p, const int32_t *alist, const int32_t *acount,
                           int logH, int SW, int32_t *gslab, int64_t slab_ints, int grid_cap, cudaStream_t st) {
-  if (p.scr == SCR_Q15) {  // K <= 32, rows of 2 or 3 16-byte chunks; checked at the entry
-    if (p.nvq == 2)
-      return launch_join<G, 2, 1, GTAB, SCR_Q15>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st);
-    return launch_join<G, 3, 1, GTAB, SCR_Q15>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st);
-  }
-  if (p.scr == SCR_Q23) {  // K <= 32, rows of 2, 3 or 4 16-byte chunks; checked at the entry
+  if (p.scr == SCR_Q23) {  // K <= 32, rows of 1 to 4 16-byte chunks; checked at the entry
+    if (p.nvq == 1)
+      return launch_join<G, 1, 1, GTAB, SCR_Q23>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st);
     if (p.nvq == 2)
       return launch_join<G, 2, 1, GTAB, SCR_Q23>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st);
     if (p.nvq == 3)
@@ -1863,11 +1774,8 @@ static int dispatch_block(const Plan &P, const JoinParams &p, const int32_t *ali
 
 static int dispatch_warp(const Plan &P, const JoinParams &p, const int32_t *alist, const int32_t *acount, int logH,
                          int SW, cudaStream_t st) {
-  if (p.scr == SCR_Q15) {
-    if (p.nvq == 2) return launch_warp<2, 1, SCR_Q15>(p, alist, acount, logH, SW, st);
-    return launch_warp<3, 1, SCR_Q15>(p, alist, acount, logH, SW, st);
-  }
   if (p.scr == SCR_Q23) {
+    if (p.nvq == 1) return launch_warp<1, 1, SCR_Q23>(p, alist, acount, logH, SW, st);
     if (p.nvq == 2) return launch_warp<2, 1, SCR_Q23>(p, alist, acount, logH, SW, st);
     if (p.nvq == 3) return launch_warp<3, 1, SCR_Q23>(p, alist, acount, logH, SW, st);
     return launch_warp<4, 1, SCR_Q23>(p, alist, acount, logH, SW, st);
@@ -2097,25 +2005,15 @@ int knnd_local_join_peers(const double *points, const float *log32, const double
   p.d64 = d;
   p.pstride = d;
   p.aside32 = nullptr;
-  if (qrows && (flags & KNND_JOIN_Q23)) {  // the 23-bit fixed-point screen (knnd_kl_q23_prepare)
-    KNND_CHECK_ARG(q_h && (q_ld == 32 || q_ld == 48 || q_ld == 64) && q_ld >= 3 * d && k <= 32,
-                   "knnd_local_join: the q23 screen needs q_h, rows of 32, 48 or 64 bytes (>= 3 d) and K <= 32 "
+  if (qrows) {  // the 23-bit fixed-point screen (knnd_kl_q23_prepare)
+    KNND_CHECK_ARG(q_h && (q_ld == 16 || q_ld == 32 || q_ld == 48 || q_ld == 64) && q_ld >= 3 * d && k <= 32,
+                   "knnd_local_join: the q23 screen needs q_h, rows of 16, 32, 48 or 64 bytes (>= 3 d) and K <= 32 "
                    "(q_ld=%d d=%d K=%d)",
                    q_ld, d, k);
-    p.l32 = log32;
     p.log32 = reinterpret_cast<const float *>(qrows);
     p.qh = q_h;
     p.nvq = q_ld / 16;
     p.scr = SCR_Q23;
-  } else if (qrows) {  // the 15-bit fixed-point screen (knnd_kl_q15_prepare)
-    KNND_CHECK_ARG(q_h && (q_ld == 16 || q_ld == 24) && q_ld >= d && k <= 32,
-                   "knnd_local_join: the q15 screen needs q_h, q_ld 16 or 24 (>= d) and K <= 32 (q_ld=%d K=%d)",
-                   q_ld, k);
-    p.l32 = log32;
-    p.log32 = reinterpret_cast<const float *>(qrows);
-    p.qh = q_h;
-    p.nvq = q_ld / 8;
-    p.scr = SCR_Q15;
   }
   if (int rc = set_peers(p, "knnd_local_join", peer_tables, npeers)) return rc;
   return join_run("knnd_local_join", p, n, d, k, row_lo, row_hi, max_indeg, ws, ws_bytes, stream, side_stream);

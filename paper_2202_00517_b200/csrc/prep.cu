@@ -32,12 +32,7 @@ __global__ void kl_prepare_kernel(const double *__restrict__ pts, int64_t n, int
   }
 }
 
-// The 15-bit fixed-point log table of the join's screen for tables larger than
-// L2 (join.cu, Q15): per column j, L0_j = min log, h_j = (max - min) / 32767
-// (0 for a constant column), q = round((log - L0_j) / h_j), stored as
-// 0x8000 | q so that the screen builds the float 1 + q 2^-15 with one byte
-// permute.  |log - (L0_j + h_j q)| <= h_j / 2.  Rows of ld16 entries (zero
-// padded; 16-byte rows).  qh[j] = (float)h_j.
+// column minima / maxima of the log table (the Q23 screen's quantisation ranges)
 __device__ __forceinline__ unsigned long long ord_f64(double v) {
   const unsigned long long b = (unsigned long long)__double_as_longlong(v);
   return b ^ ((unsigned long long)((long long)b >> 63) | 0x8000000000000000ull);
@@ -60,30 +55,6 @@ __global__ void col_minmax_kernel(const double *__restrict__ log64, int64_t n, i
   }
   atomicMin(mm + j, lo);
   atomicMax(mm + d + j, hi);
-}
-
-__global__ void q15_quantize_kernel(const double *__restrict__ log64, int64_t n, int d, int ld16,
-                                    const unsigned long long *__restrict__ mm, uint16_t *__restrict__ q15,
-                                    float *__restrict__ qh) {
-  const int64_t total = n * ld16;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / ld16;
-    const int j = (int)(i - r * ld16);
-    unsigned q = 0;
-    if (j < d) {
-      const double lo = unord_f64(mm[j]), hi = unord_f64(mm[d + j]);
-      const double h = (hi - lo) / 32767.0;
-      if (h > 0.0) {
-        double t = rint((log64[r * d + j] - lo) / h);
-        t = t < 0.0 ? 0.0 : (t > 32767.0 ? 32767.0 : t);
-        q = (unsigned)t;
-      }
-      if (r == 0) qh[j] = (float)h;
-    } else if (r == 0) {
-      qh[j] = 0.f;
-    }
-    q15[i] = (uint16_t)(0x8000u | q);
-  }
 }
 
 // The 23-bit fixed-point log table of the join's Q23 screen (join.cu): per
@@ -312,30 +283,7 @@ int knnd_kl_prepare(const double *points, int64_t n, int32_t d, int32_t ld32, fl
   return KNND_OK;
 }
 
-size_t knnd_kl_q15_workspace_bytes(int32_t d) { return d < 1 ? 0 : align_up((size_t)d * 16, 256); }
-
-int knnd_kl_q15_prepare(const double *log64, int64_t n, int32_t d, int32_t ld16, uint16_t *q15, float *qh, void *ws,
-                        size_t ws_bytes, void *stream) {
-  KNND_CHECK_ARG(log64 && q15 && qh, "knnd_kl_q15_prepare: null pointer");
-  KNND_CHECK_ARG(n >= 1 && d >= 1 && d <= 256, "knnd_kl_q15_prepare: bad shape n=%lld d=%d", (long long)n, d);
-  KNND_CHECK_ARG(ld16 >= d && ld16 % 8 == 0, "knnd_kl_q15_prepare: ld16=%d must be >= d and a multiple of 8", ld16);
-  if (!ws || ws_bytes < knnd_kl_q15_workspace_bytes(d)) {
-    set_error("knnd_kl_q15_prepare: workspace %zu < %zu bytes", ws_bytes, knnd_kl_q15_workspace_bytes(d));
-    return KNND_EWORKSPACE;
-  }
-  cudaStream_t st = as_stream(stream);
-  unsigned long long *mm = static_cast<unsigned long long *>(ws);
-  KNND_CUDA(cudaMemsetAsync(mm, 0xFF, (size_t)d * 8, st));
-  KNND_CUDA(cudaMemsetAsync(mm + d, 0x00, (size_t)d * 8, st));
-  const int threads = (256 / d) * d > 0 ? (256 / d) * d : d;
-  col_minmax_kernel<<<num_sms() * 4, threads, 0, st>>>(log64, n, d, mm);
-  KNND_LAUNCHED(1);
-  int64_t blocks = (n * ld16 + 255) / 256;
-  if (blocks > (int64_t)num_sms() * 32) blocks = (int64_t)num_sms() * 32;
-  q15_quantize_kernel<<<(unsigned)blocks, 256, 0, st>>>(log64, n, d, ld16, mm, q15, qh);
-  KNND_LAUNCHED(1);
-  return KNND_OK;
-}
+size_t knnd_kl_q23_workspace_bytes(int32_t d) { return d < 1 ? 0 : align_up((size_t)d * 16, 256); }
 
 int knnd_kl_q23_prepare(const double *log64, int64_t n, int32_t d, int32_t row_bytes, uint8_t *q23, float *qh,
                         void *ws, size_t ws_bytes, void *stream) {
@@ -343,8 +291,8 @@ int knnd_kl_q23_prepare(const double *log64, int64_t n, int32_t d, int32_t row_b
   KNND_CHECK_ARG(n >= 1 && d >= 1 && d <= 256, "knnd_kl_q23_prepare: bad shape n=%lld d=%d", (long long)n, d);
   KNND_CHECK_ARG(row_bytes >= 3 * d && row_bytes % 16 == 0,
                  "knnd_kl_q23_prepare: row_bytes=%d must be >= 3 d and a multiple of 16", row_bytes);
-  if (!ws || ws_bytes < knnd_kl_q15_workspace_bytes(d)) {
-    set_error("knnd_kl_q23_prepare: workspace %zu < %zu bytes", ws_bytes, knnd_kl_q15_workspace_bytes(d));
+  if (!ws || ws_bytes < knnd_kl_q23_workspace_bytes(d)) {
+    set_error("knnd_kl_q23_prepare: workspace %zu < %zu bytes", ws_bytes, knnd_kl_q23_workspace_bytes(d));
     return KNND_EWORKSPACE;
   }
   cudaStream_t st = as_stream(stream);

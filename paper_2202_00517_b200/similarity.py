@@ -106,7 +106,7 @@ def upload(host: np.ndarray, device: torch.device) -> torch.Tensor:
     return out
 
 
-Q15_MIN_BYTES = 96 << 20  # fp32 screen tables above this (of a 126 MB L2) take the 15-bit screen
+Q23_MAX_ROW_BYTES = 64  # the join's Q23 screen is built for rows of 16 / 32 / 48 / 64 bytes (d <= 5 / 10 / 16 / 21)
 
 
 def _dev(device) -> torch.device:
@@ -140,56 +140,34 @@ class DeviceTables:
         _lib.call("knnd_kl_prepare", self.points.data_ptr(), self.n, self.d, self.ld, self.log32.data_ptr(),
                   self.log64.data_ptr(), self.xlogx.data_ptr(), _stream(device))
         self.dplan = self.d  # the screen row width the join plans for
-        # the join's 15-bit screen for tables larger than L2 (knnd_kl_q15_prepare):
-        # the random row gather is DRAM-bound there and 48-byte rows move faster
-        # than 80-byte ones; results do not depend on it (KNND_Q15=0/1 forces it)
-        self.q15 = self.qh = None
-        self.ld16 = (self.d + 7) // 8 * 8
-        # the join's 23-bit screen (knnd_kl_q23_prepare): 3 bytes per entry, rows of
-        # 32 / 48 / 64 bytes (d <= 10 / 16 / 21) — at d = 20 two aligned sectors in
-        # one 128-B line per row instead of three sectors over 1.5 lines, with an
-        # error bound as tight as the fp32 screen's.  KNND_Q23=0/1 forces it off / on.
+        # The join's 23-bit fixed-point screen (knnd_kl_q23_prepare): 3 bytes per entry,
+        # rows of 16 to 64 bytes — at d = 20 two aligned sectors in one 128-byte
+        # line per row instead of three sectors over 1.5 lines.  The random row gather
+        # sets the join's rate (tools/row_probe.cu), the error bound is as tight as
+        # the fp32 screen's, and results do not depend on it (KNND_Q23=0 keeps the
+        # fp32 rows).  Not built when a log is not finite (a zero coordinate).
         self.q23 = self.qh23 = None
         self.q23_bytes = (3 * self.d + 15) // 16 * 16
-        force23 = os.environ.get("KNND_Q23")
-        if force23 == "1" and self.q23_bytes <= 64:
+        if os.environ.get("KNND_Q23", "1") != "0" and self.q23_bytes <= Q23_MAX_ROW_BYTES:
             self.q23 = torch.empty((self.n, self.q23_bytes), dtype=torch.uint8, device=device)
             self.qh23 = torch.empty(self.q23_bytes // 3, dtype=torch.float32, device=device)
-            ws = torch.empty(max(int(_lib.load().knnd_kl_q15_workspace_bytes(self.d)), 256), dtype=torch.uint8,
+            ws = torch.empty(max(int(_lib.load().knnd_kl_q23_workspace_bytes(self.d)), 256), dtype=torch.uint8,
                              device=device)
             _lib.call("knnd_kl_q23_prepare", self.log64.data_ptr(), self.n, self.d, self.q23_bytes,
                       self.q23.data_ptr(), self.qh23.data_ptr(), ws.data_ptr(), ws.numel(), _stream(device))
-            if not bool(torch.isfinite(self.qh23).all().item()):  # a non-finite log: keep the fp32 screen
+            if not bool(torch.isfinite(self.qh23).all().item()):  # (synchronises: ws is a temporary)
                 self.q23 = self.qh23 = None
-        force = os.environ.get("KNND_Q15")
-        want = force == "1" or (force is None and self.n * self.ld * 4 > Q15_MIN_BYTES)
-        if want and self.ld16 in (16, 24) and self.q23 is None:
-            self.q15 = torch.empty((self.n, self.ld16), dtype=torch.int16, device=device)
-            self.qh = torch.empty(self.ld16, dtype=torch.float32, device=device)
-            ws = torch.empty(max(int(_lib.load().knnd_kl_q15_workspace_bytes(self.d)), 256), dtype=torch.uint8,
-                             device=device)
-            _lib.call("knnd_kl_q15_prepare", self.log64.data_ptr(), self.n, self.d, self.ld16, self.q15.data_ptr(),
-                      self.qh.data_ptr(), ws.data_ptr(), ws.numel(), _stream(device))
-            torch.cuda.current_stream(device).synchronize()  # ws is a temporary
 
     # -- the kernel calls (one per ABI entry; the L2 tables provide the same methods)
     def join(self, table, k, csr, max_indeg, out_rows, tally, out_scores, out_ucount, bound_in, bound_out, ws,
              flags, stream, peers=(), side_stream=None):
-        q15 = self.q15 is not None and k <= 32  # (the same choice every round of a descent: K is fixed)
-        if self.q23 is not None and k <= 32:
-            _lib.call("knnd_local_join_peers", self.points.data_ptr(), self.log32.data_ptr(), self.log64.data_ptr(),
-                      self.xlogx.data_ptr(), self.n, self.d, self.ld, table.data_ptr(), k, csr.indptr.data_ptr(),
-                      csr.indices.data_ptr(), csr.lo, csr.hi, max_indeg, out_rows.data_ptr(), _ptr(out_scores),
-                      _ptr(out_ucount), tally.data_ptr(), _ptr(bound_in), _ptr(bound_out), ws.data_ptr(), ws.numel(),
-                      flags | _lib.JOIN_Q23, _lib.peer_array(peers), len(peers), self.q23.data_ptr(),
-                      self.qh23.data_ptr(), self.q23_bytes, stream, side_stream)
-            return
+        q23 = self.q23 is not None and k <= 32  # (the same choice every round of a descent: K is fixed)
         _lib.call("knnd_local_join_peers", self.points.data_ptr(), self.log32.data_ptr(), self.log64.data_ptr(),
                   self.xlogx.data_ptr(), self.n, self.d, self.ld, table.data_ptr(), k, csr.indptr.data_ptr(),
                   csr.indices.data_ptr(), csr.lo, csr.hi, max_indeg, out_rows.data_ptr(), _ptr(out_scores),
                   _ptr(out_ucount), tally.data_ptr(), _ptr(bound_in), _ptr(bound_out), ws.data_ptr(), ws.numel(),
-                  flags, _lib.peer_array(peers), len(peers), _ptr(self.q15) if q15 else None,
-                  _ptr(self.qh) if q15 else None, self.ld16 if q15 else 0, stream, side_stream)
+                  flags, _lib.peer_array(peers), len(peers), _ptr(self.q23) if q23 else None,
+                  _ptr(self.qh23) if q23 else None, self.q23_bytes if q23 else 0, stream, side_stream)
 
     def join_flags(self) -> int:
         return _lib.JOIN_NONPOS_LOG if self.max_coord <= 1.0 else 0

@@ -58,7 +58,7 @@ def test_library_is_sm100a_code():
 
 
 def test_version_and_counter(lib):
-    assert lib.knnd_abi_version() == 2
+    assert lib.knnd_abi_version() == 3
     assert b2.launch_count() >= 0
 
 

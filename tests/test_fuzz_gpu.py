@@ -1,7 +1,7 @@
 """Randomised parity sweep: full descents on the device against the C oracle
 (pinned to the reference in tests/test_oracle.py) over seeded random shapes —
 n from 60 to 30k, d from 2 to 60, K from 2 to 64, simplex (KL) and Gaussian
-(squared Euclidean) data, with the Q15 screen forced on for part of the KL
+(squared Euclidean) data, with the Q23 screen on for part of the KL
 cases, and data with duplicated points (exact score ties).  Every round's
 table must equal the oracle's exactly (the order contract leaves no freedom:
 ties go to the lower id), with the same comparisons, changed rows and FCC
@@ -27,25 +27,25 @@ def _cases():
         n = int(rng.integers(max(3 * k, 60), 30_000))
         d = int(rng.choice([2, 3, 5, 7, 10, 16, 20, 24, 33, 50, 60]))
         metric = "kl" if i % 3 else "l2"
-        q15 = metric == "kl" and i % 2 == 0 and d <= 24 and k <= 32 and d > 8
+        q23 = metric == "kl" and i % 2 == 0 and d <= 21 and k <= 32
         dup = i % 5 == 4
-        out.append((i, n, d, k, metric, q15, dup))
+        out.append((i, n, d, k, metric, q23, dup))
     # edge-heavy shapes: tiny K, n barely above K, one- and two-dimensional data
     # (d = 1 KL: every point is 1.0, every score ties), many duplicates
-    for j, (n, d, k, metric, q15, dup) in enumerate([
-            (7, 3, 2, "kl", False, False), (40, 1, 3, "kl", False, False), (300, 2, 2, "kl", False, True),
+    for j, (n, d, k, metric, q23, dup) in enumerate([
+            (7, 3, 2, "kl", True, False), (40, 1, 3, "kl", True, False), (300, 2, 2, "kl", False, True),
             (2000, 12, 2, "kl", True, True), (5000, 20, 3, "kl", True, True), (65, 5, 64, "kl", False, False),
             (3000, 1, 4, "l2", False, False), (4000, 2, 2, "l2", False, True), (20000, 9, 64, "l2", False, True),
             (25000, 16, 32, "kl", True, True), (1200, 60, 64, "kl", False, True), (600, 33, 20, "l2", False, False)]):
-        out.append((100 + j, n, d, k, metric, q15, dup))
+        out.append((100 + j, n, d, k, metric, q23, dup))
     return out
 
 
 @pytest.mark.parametrize("case", _cases(), ids=lambda c: f"c{c[0]}_n{c[1]}_d{c[2]}_k{c[3]}_{c[4]}"
-                         + ("_q15" if c[5] else "") + ("_dup" if c[6] else ""))
+                         + ("_q23" if c[5] else "") + ("_dup" if c[6] else ""))
 def test_descent_matches_oracle(cuda, monkeypatch, case):
-    i, n, d, k, metric, q15, dup = case
-    monkeypatch.setenv("KNND_Q15", "1" if q15 else "0")
+    i, n, d, k, metric, q23, dup = case
+    monkeypatch.setenv("KNND_Q23", "1" if q23 else "0")
     rng = np.random.default_rng(1000 + i)
     if metric == "kl":
         pts = port.simplex_points(d, n, rng)

@@ -377,7 +377,7 @@ def test_c4_trajectory(cuda, trajectories):
 @pytest.mark.slow
 def test_c5_trajectory(cuda, trajectories):
     """C5, n = 10M, d = 20, K = 20 (the scaling-stress config, 800 MB fp32 log
-    table, the Q15 screen): the initial table and both rounds' tables equal
+    table, the Q23 screen): the initial table and both rounds' tables equal
     the reference's recorded ones (sha256), with its comparisons, changed rows
     and FCC counts, and the descent stops at the same round (2).  Recall of the
     final table on the reference's 10,000-id sample, exact rows by the GPU

@@ -1,8 +1,9 @@
 """The join's 23-bit fixed-point screen (knnd_kl_q23_prepare + the q23 path of
-knnd_local_join_peers: 3 bytes per entry, 64-byte rows at d = 20), forced on
-(KNND_Q23=1).  The screen only prunes candidates (with a rigorous error bound
-of the fp32 screen's form) and orders certified rows; the fp64 decision is
-unchanged, so every table must equal the reference's / the oracle's exactly."""
+knnd_local_join_peers: 3 bytes per entry, 64-byte rows at d = 20; on by
+default for d <= 21, K <= 32) and the fp32 screen it replaces (KNND_Q23=0).
+Either screen only prunes candidates (with a rigorous error bound) and orders
+certified rows; the fp64 decision is unchanged, so every table must equal the
+reference's / the oracle's exactly with both."""
 
 from __future__ import annotations
 
@@ -22,6 +23,12 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture
 def q23_on(monkeypatch):
     monkeypatch.setenv("KNND_Q23", "1")
+
+
+@pytest.fixture(params=["q23", "fp32"])
+def screen(request, monkeypatch):
+    monkeypatch.setenv("KNND_Q23", "1" if request.param == "q23" else "0")
+    return request.param
 
 
 def test_q23_table_quantisation(cuda, q23_on):
@@ -54,7 +61,7 @@ def test_q23_non_finite_logs_keep_fp32(cuda, q23_on):
 
 
 @pytest.mark.parametrize("name", ["n1000_d20_k20_s1", "n1500_d16_k10_s7", "n800_d10_k40_s5"])
-def test_q23_small_trajectories(cuda, q23_on, small_meta, name):
+def test_q23_small_trajectories(cuda, screen, small_meta, name):
     """Full descents with the q23 screen reproduce the reference's per-round
     tables (d = 20, 16, 10: rows of 64 / 48 / 32 bytes; K = 40 > 32 takes the fp32 screen)."""
     meta = small_meta[name]
@@ -67,14 +74,14 @@ def test_q23_small_trajectories(cuda, q23_on, small_meta, name):
     assert sha_i32(friends) == meta["rounds"][-1]["sha"]
 
 
-def test_q23_c2_trajectory(cuda, q23_on, trajectories):
+def test_q23_c2_trajectory(cuda, screen, trajectories):
     """C2 (n = 100k, d = 10, K = 20) with the q23 screen: every round's table sha,
     comparisons, changed rows and FCC count equal the reference's."""
     ref = trajectories["c2"]
     n, d, k, seed = ref["n"], ref["d"], ref["k"], ref["seed"]
     pts = port.experiment_points(n, d, seed)
     rs = b2.KlRankingSystem(pts, validate=False)
-    assert rs.device_tables().q23 is not None
+    assert (rs.device_tables().q23 is not None) == (screen == "q23")
     cfg = b2.DescentConfig(k=k, seed=seed)
     st = b2.init_random_kout(b2.Dataset(pts), rs, cfg, b2.derive_rng(seed, 2))
     for r in ref["rounds"]:
@@ -84,7 +91,7 @@ def test_q23_c2_trajectory(cuda, q23_on, trajectories):
             (r["comparisons"], r["changed"], r["fcc_count"])
 
 
-def test_q23_size_classes_and_hubs_vs_oracle(cuda, q23_on):
+def test_q23_size_classes_and_hubs_vs_oracle(cuda, screen):
     """Every size class (warp, 128/256/512-thread blocks, global-memory hubs)
     through the q23 screen: rows and |U| equal the C oracle's."""
     from test_gpu import _hub_table
@@ -97,7 +104,7 @@ def test_q23_size_classes_and_hubs_vs_oracle(cuda, q23_on):
     rs = b2.KlRankingSystem(pts, validate=False)
     st = b2.KnnState(table)
     tabs = rs.device_tables()
-    assert tabs.q23 is not None
+    assert (tabs.q23 is not None) == (screen == "q23")
     out = torch.empty((n, k), dtype=torch.int32, device=cuda)
     uc = torch.empty(n, dtype=torch.int32, device=cuda)
     tally = torch.zeros(4, dtype=torch.int64, device=cuda)

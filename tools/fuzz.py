@@ -21,9 +21,9 @@ for i in range(count):
     n = int(rng.integers(k + 2, int(rng.choice([200, 5000, 60000, 200000]))))
     d = int(rng.integers(1, 70))
     metric = "kl" if rng.random() < 0.7 else "l2"
-    q15 = metric == "kl" and rng.random() < 0.4
+    q23 = metric == "kl" and rng.random() < 0.6
     dup = rng.random() < 0.3
-    os.environ["KNND_Q15"] = "1" if q15 else "0"
+    os.environ["KNND_Q23"] = "1" if q23 else "0"
     r = np.random.default_rng(seed0 * 1000 + i)
     try:
         if metric == "kl":
@@ -50,7 +50,7 @@ for i in range(count):
     except Exception:
         ok = False
         traceback.print_exc()
-    tag = f"case {i}: n={n} d={d} k={k} {metric}{' q15' if q15 else ''}{' dup' if dup else ''}"
+    tag = f"case {i}: n={n} d={d} k={k} {metric}{' q23' if q23 else ''}{' dup' if dup else ''}"
     if not ok:
         bad += 1
         print("MISMATCH", tag, flush=True)

@@ -17,7 +17,7 @@ summ bench_b256 "B256 (2^14 table) join launch, C3 bench step"
 C5="python bench.py --config c5 --steps 1 --warmup 1 --e2e-steps 0 --no-cpu-baseline --no-clocks --no-recall"
 $C5 > gpurun_out/bench_c5_short.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:join_warp_kernel -s 2 -c 1 -o gpurun_out/bench_c5_w1 $C5 > gpurun_out/ncu_c5.log 2>&1
-summ bench_c5_w1 "C5 W1 join launch (Q15 screen), bench step"
+summ bench_c5_w1 "C5 W1 join launch (Q23 screen), bench step"
 python tools/exact_probe.py 1000000 20 20 100000 > gpurun_out/exact_plain.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:exact_tc -s 1 -c 1 -o gpurun_out/exact_tc \
     python tools/exact_probe.py 1000000 20 20 100000 > gpurun_out/ncu_exact.log 2>&1
