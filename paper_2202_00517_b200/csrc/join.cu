@@ -147,9 +147,24 @@ __device__ __forceinline__ void hash_insert4(int32_t *table, const int (&id)[UNR
     nw[u] = can && prev[u] == EMPTY;
     retry[u] = valid[u] && !found && !nw[u] && prev[u] != y;
   }
+  // the retries of a lane run one after the other inside ONE divergent region
+  // (lanes with no retry skip it), not as UNR1 regions one after the other: in
+  // a pass of 32 x UNR1 ids some lane nearly always loses a slot to another
+  // id of the same bucket, and the warp then pays for the longest lane, not
+  // for the sum over u of the longest lanes
+  unsigned pend = 0;
 #pragma unroll
-  for (int u = 0; u < UNR1; ++u)
-    if (retry[u]) nw[u] = hash_insert_cas(table, id[u], shift, mask);
+  for (int u = 0; u < UNR1; ++u) pend |= retry[u] ? 1u << u : 0u;
+  while (pend) {
+    const int u = __ffs(pend) - 1;
+    pend &= pend - 1;
+    int y = id[0];
+#pragma unroll
+    for (int q = 1; q < UNR1; ++q) y = u == q ? id[q] : y;
+    const bool isnew = hash_insert_cas(table, y, shift, mask);
+#pragma unroll
+    for (int q = 0; q < UNR1; ++q) nw[q] = u == q ? isnew : nw[q];
+  }
 }
 
 // warp-aggregated append of `val` (where `take`) to list[*counter ...]
