@@ -1116,7 +1116,7 @@ struct WarpSlab {
   size_t x32, x64, S, pre, table, list, total;  // (x32, x64, S) twice, `pre` bytes apart
 };
 
-__host__ __device__ inline WarpSlab warp_slab(int d, int ld, int H, int SW) {
+__host__ __device__ inline WarpSlab warp_slab(int d, int ld, int H, int SW, int cap) {
   WarpSlab L;
   size_t o = 0;
   L.x32 = o;
@@ -1130,7 +1130,7 @@ __host__ __device__ inline WarpSlab warp_slab(int d, int ld, int H, int SW) {
   L.table = o;
   o = al16(o + (size_t)H * 4);
   L.list = o;
-  o = al16(o + (size_t)(H / 2) * 4);
+  o = al16(o + (size_t)cap * 4);  // the unique list: up to `cap` ids (the class's pre-dedup bound)
   L.total = o;
   return L;
 }
@@ -1154,14 +1154,14 @@ __device__ __forceinline__ void prefetch_anchor(const JoinParams &p, int x, int6
 template <int NV4, int KPL, bool VF, int SCR>
 __global__ void __launch_bounds__(128, 4)
     join_warp_kernel(JoinParams p, const int32_t *__restrict__ alist, const int32_t *__restrict__ acount, int logH,
-                     int SW) {
+                     int SW, int cap) {
   constexpr int Q = 2 * KPL;  // per-lane kept screened values
   constexpr bool Q23S = SCR == SCR_Q23;
   extern __shared__ __align__(16) unsigned char sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int H = 1 << logH;
   const unsigned shift = 32u - (unsigned)logH;
-  const WarpSlab L = warp_slab(p.d, p.ld, H, SW);
+  const WarpSlab L = warp_slab(p.d, p.ld, H, SW, cap);
   unsigned char *base = sm + (size_t)warp * L.total;
   int32_t *table = reinterpret_cast<int32_t *>(base + L.table);
   int32_t *list = reinterpret_cast<int32_t *>(base + L.list);
@@ -1296,7 +1296,7 @@ __global__ void __launch_bounds__(128, 4)
           KNND_DCHECK(!nw[u] || (id[u] >= 0 && id[u] < p.n));
           if (nw[u]) list[U + __popc(m & lanemask_lt())] = id[u];
           U += __popc(m);
-          KNND_DCHECK(U <= (H >> 1));
+          KNND_DCHECK(U <= cap);
         }
       }
     } else {
@@ -1348,7 +1348,7 @@ __global__ void __launch_bounds__(128, 4)
           KNND_DCHECK(!nw[u] || (id[u] >= 0 && id[u] < p.n));
           if (nw[u]) list[U + __popc(m & lanemask_lt())] = id[u];
           U += __popc(m);
-          KNND_DCHECK(U <= (H >> 1));
+          KNND_DCHECK(U <= cap);
         }
       }
     }
@@ -1553,6 +1553,7 @@ enum { KIND_WARP = 0, KIND_BLOCK128 = 1, KIND_BLOCK256 = 2, KIND_GLOBAL = 3, KIN
 
 struct Cls {
   int kind, logH, sw;
+  int cap;      // warp class: capacity of the unique list (= lim)
   int64_t lim;  // pre-dedup bound handled (H/2 for shared-memory tables)
   bool need;
 };
@@ -1649,13 +1650,22 @@ static Plan make_plan(int64_t n_items, int64_t m, int d, int K, int max_indeg) {
     c.kind = kind[i];
     c.logH = logH[i];
     c.lim = ((int64_t)1 << c.logH) / 2;
+    // the warp class fills its table past one half (4-slot buckets take it): its
+    // slab has room for a longer unique list, and warp anchors run ~35% faster
+    // than the 2^12 block class they would otherwise join (KNND_WLIM overrides)
+    if (c.kind == KIND_WARP && i == 0) {
+      int64_t wl = c.lim * 5 / 4;
+      if (const char *env = getenv("KNND_WLIM")) wl = atoll(env);
+      if (wl >= c.lim && wl <= c.lim * 11 / 8) c.lim = wl;
+    }
+    c.cap = (int)c.lim;
     c.sw = (int)(c.lim / K1 + 1);
     // a shared-memory class must fit: the staged S list (up to lim / (K + 1)
     // ids, double-buffered) grows as K shrinks (K = 2: a third of the table);
     // the classes from the first that does not fit on are left to the
     // global-memory class, whose S and table live in its slab
     const size_t need = c.kind == KIND_WARP
-                            ? warp_slab(d, ld, 1 << c.logH, c.sw).total
+                            ? warp_slab(d, ld, 1 << c.logH, c.sw, c.cap).total
                             : smem_layout(c.kind == KIND_BLOCK128 ? 128 : c.kind == KIND_BLOCK256 ? 256 : 512, false,
                                           d, ld, 1 << c.logH, c.sw)
                                   .total;
@@ -1730,10 +1740,10 @@ static int launch_join(const JoinParams &p, const int32_t *alist, const int32_t 
 
 template <int NV4, int KPL, int SCR = SCR_F32>
 static int launch_warp(const JoinParams &p, const int32_t *alist, const int32_t *acount, int logH, int SW,
-                       cudaStream_t st) {
+                       int cap, cudaStream_t st) {
   // friend rows as int4 when they are 16-B aligned (K % 4 == 0)
   auto kern = (p.K % 4 == 0) ? join_warp_kernel<NV4, KPL, true, SCR> : join_warp_kernel<NV4, KPL, false, SCR>;
-  const WarpSlab L = warp_slab(p.d, p.ld, 1 << logH, SW);
+  const WarpSlab L = warp_slab(p.d, p.ld, 1 << logH, SW, cap);
   // warps per block: the largest of 4/2/1 that keeps the most warps resident
   // (big tables leave room for fewer than 4 slabs per block slot)
   int best_wpb = 0, best_warps = 0;
@@ -1753,7 +1763,7 @@ static int launch_warp(const JoinParams &p, const int32_t *alist, const int32_t 
     set_error("local join: warp slabs %zu B exceed 227 KB (d=%d, H=%d)", L.total, p.d, 1 << logH);
     return KNND_EUNSUPPORTED;
   }
-  kern<<<(best_warps / best_wpb) * num_sms(), best_wpb * 32, smem, st>>>(p, alist, acount, logH, SW);
+  kern<<<(best_warps / best_wpb) * num_sms(), best_wpb * 32, smem, st>>>(p, alist, acount, logH, SW, cap);
   KNND_LAUNCHED(1);
   return KNND_OK;
 }
@@ -1788,16 +1798,16 @@ static int dispatch_block(const Plan &P, const JoinParams &p, const int32_t *ali
 }
 
 static int dispatch_warp(const Plan &P, const JoinParams &p, const int32_t *alist, const int32_t *acount, int logH,
-                         int SW, cudaStream_t st) {
+                         int SW, int cap, cudaStream_t st) {
   if (p.scr == SCR_Q23) {
-    if (p.nvq == 1) return launch_warp<1, 1, SCR_Q23>(p, alist, acount, logH, SW, st);
-    if (p.nvq == 2) return launch_warp<2, 1, SCR_Q23>(p, alist, acount, logH, SW, st);
-    if (p.nvq == 3) return launch_warp<3, 1, SCR_Q23>(p, alist, acount, logH, SW, st);
-    return launch_warp<4, 1, SCR_Q23>(p, alist, acount, logH, SW, st);
+    if (p.nvq == 1) return launch_warp<1, 1, SCR_Q23>(p, alist, acount, logH, SW, cap, st);
+    if (p.nvq == 2) return launch_warp<2, 1, SCR_Q23>(p, alist, acount, logH, SW, cap, st);
+    if (p.nvq == 3) return launch_warp<3, 1, SCR_Q23>(p, alist, acount, logH, SW, cap, st);
+    return launch_warp<4, 1, SCR_Q23>(p, alist, acount, logH, SW, cap, st);
   }
 #define KNND_CALL(NV)                                                             \
-  return P.kpl == 1 ? launch_warp<NV, 1>(p, alist, acount, logH, SW, st) \
-                    : launch_warp<NV, 2>(p, alist, acount, logH, SW, st)
+  return P.kpl == 1 ? launch_warp<NV, 1>(p, alist, acount, logH, SW, cap, st) \
+                    : launch_warp<NV, 2>(p, alist, acount, logH, SW, cap, st)
   KNND_NV_SWITCH(KNND_CALL)
 #undef KNND_CALL
 }
@@ -1809,7 +1819,7 @@ static int dispatch_class(const Plan &P, int i, const JoinParams &p, const int32
   const int32_t *acount = counts + i;
   switch (c.kind) {
     case KIND_WARP:
-      return dispatch_warp(P, p, alist, acount, c.logH, c.sw, st);
+      return dispatch_warp(P, p, alist, acount, c.logH, c.sw, c.cap, st);
     case KIND_BLOCK128:
       return dispatch_block<128, false>(P, p, alist, acount, c.logH, c.sw, nullptr, 0, 0, st);
     case KIND_BLOCK256:
