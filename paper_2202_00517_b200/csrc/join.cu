@@ -342,7 +342,7 @@ __device__ __forceinline__ void screen_row_reg(const float *row, const float4 (&
 // value v = sum_j w_j F_j = 2^-23 sum_j x_j h_j q_j equals
 // 2^-23 (ce + sum_j x_j Lmax_j) up to
 //   quantisation            2^-23 A1 / 2,  A1 = sum_j x_j h_j   (|q - exact| <= 1/2)
-//   fp32 weights and FMAs   (NQ + 12) 2^-24 v                    (every term >= 0: x_j > 0)
+//   fp32 weights and FMAs   (ceil(NQ / 4) + 6) 2^-24 v           (every term >= 0: x_j > 0)
 // — the fp32 screen's error model (relative band on max v, plus an absolute
 // slack), so the threshold / certification rules are shared with it and the
 // fp64 ranking is the only second tier.
@@ -498,7 +498,7 @@ __device__ __forceinline__ bool certify_row(const JoinParams &p, const int32_t *
   key = warp_sort32(key, lane);
   const float kv = key.v();
   const float nextv = __shfl_down_sync(FULL, kv, 1);
-  const float gap_need = band + fabsf(kv) * 2e-6f + 1e-30f;
+  const float gap_need = band + fabsf(kv) * 2.5e-7f + 1e-30f;  // (the margin: ~4 ulp for the gap arithmetic)
   const bool need_check = lane < K && lane + 1 < nR;  // nR == K: the set is R itself
   const bool ok = !need_check || (nextv - kv > gap_need);
   if (!__all_sync(FULL, ok)) return false;
@@ -1061,6 +1061,11 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     }
     const float ebase = p.band * am + slack;  // the screen's error bound at this anchor
     const float theta = T + 2.f * ebase + fabsf(T) * 1e-6f;
+    // the error bound among the members of R: a candidate's error is band * its
+    // own sum |x log y| (+ slack), which equals its screened value (<= theta)
+    // when every term has one sign — usually several times tighter than the
+    // bound over all of U, so fewer rows fall back to the fp64 ranking
+    const float ebase_r = (Q23S || p.nonpos) ? p.band * fminf(am, theta) + slack : ebase;
     if (hdr[8] < count) prefetch(pb ^ 1, hdr[9], hdr64[0], hdr[12]);
 
     // ---- phase 3: collect every candidate the screen cannot exclude
@@ -1075,7 +1080,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
       bool diff;
       float kth = theta;  // every member of the new row has a screened value <= theta
       if (!(KPL == 1 && p.out_kl == nullptr && nR <= 32 &&
-            certify_row(p, R, rval, nR, 2.f * ebase, x, xr, lane, diff, kth))) {
+            certify_row(p, R, rval, nR, 2.f * ebase_r, x, xr, lane, diff, kth))) {
         diff = exact_row<KPL>(p, R, nR, stage64, rcap64, x64, x, xr, lane);
         ++acc_exact;
       }
@@ -1470,6 +1475,11 @@ __global__ void __launch_bounds__(128, 4)
       T = lane_pair_T();
     }
     const float theta = T + 2.f * ebase + fabsf(T) * 1e-6f;
+    // the error bound among the members of R: a candidate's error is band * its
+    // own sum |x log y| (+ slack), which equals its screened value (<= theta)
+    // when every term has one sign — usually several times tighter than the
+    // bound over all of U, so fewer rows fall back to the fp64 ranking
+    const float ebase_r = (Q23S || p.nonpos) ? p.band * fminf(am, theta) + slack : ebase;
 
     // ---- phase 3: R (ids and screened values) in place at the front of list / scores
     int nR = 0;
@@ -1492,7 +1502,7 @@ __global__ void __launch_bounds__(128, 4)
     bool diff;
     float kth = theta;  // every member of the new row has a screened value <= theta
     if (!(KPL == 1 && p.out_kl == nullptr && nR <= 32 &&
-          certify_row(p, list, scores, nR, 2.f * ebase, x, xr, lane, diff, kth))) {
+          certify_row(p, list, scores, nR, 2.f * ebase_r, x, xr, lane, diff, kth))) {
       diff = exact_row<KPL>(p, list, nR, stage64, rcap64, x64, x, xr, lane);
       ++acc_exact;
     }
@@ -1885,7 +1895,9 @@ static int join_run(const char *who, JoinParams &p, int64_t n, int32_t dplan, in
   p.K = k;
   // rigorous bound on |fp32 screen - fp64| relative to sum |x*log y| (+ margin)
   p.band = (float)((ld32 + 8) * 0x1p-24);
-  if (p.scr == SCR_Q23) p.band = (float)(((16 * p.nvq) / 3 + 12) * 0x1p-24);  // NQ products, weights, chains
+  // Q23: three roundings in a weight (x, h, their product), a chain of ceil(NQ / 4)
+  // FMAs and two adds per entry — (1 + u)^(ceil(NQ / 4) + 5) - 1, one more u of margin
+  if (p.scr == SCR_Q23) p.band = (float)((((16 * p.nvq) / 3 + 3) / 4 + 6) * 0x1p-24);
 
   KNND_CUDA(cudaMemsetAsync(counts, 0, 64, st));
   {
