@@ -145,7 +145,7 @@ int knnd_local_join(const double *points, const float *log32, const double *log6
  * gathered table, the caller runs a cross-rank barrier on the stream (the
  * kernels end with a system-scope fence).  npeers in 0..KNND_MAX_PEERS.
  * qrows / q_h / q_ld (nullable qrows): screen with the 23-bit fixed-point copy
- * of the log table (knnd_kl_q23_prepare: q_ld = 16, 32, 48 or 64 bytes per row,
+ * of the log table (knnd_kl_q23_prepare: q_ld = 16, 32, 48, 64 or 160 bytes per row,
  * >= 3 d; K <= 32) instead of log32 — the random row gather sets the join's
  * rate and smaller rows move faster (64-byte rows at d = 20: two aligned
  * sectors in one 128-byte line, against three sectors over 1.5 lines); the

@@ -366,26 +366,43 @@ __device__ __forceinline__ float q23_weights(const double *x64, const float *__r
   return s * 0x1p-75f * (1.f + 0x1p-9f) + 1e-36f;  // sum_j w_j 2^-150 = 2^-23 A1 / 2
 }
 
-template <int NCH>
-__device__ __forceinline__ float screen_row_q23(const float *row, const float (&w)[Q23<NCH>::NQ]) {
-  const uint4 *r4 = reinterpret_cast<const uint4 *>(row);
-  unsigned W[4 * NCH];
+// entries [J0, J0 + NJ) of a row from the CW words at word offset W0 (48 bytes
+// hold 16 entries exactly, so 3-chunk groups are self-contained)
+template <int W0, int CW, int J0, int NJ, int NQ>
+__device__ __forceinline__ void q23_group(const float *row, const float (&w)[NQ], float (&a)[4]) {
+  const uint4 *r4 = reinterpret_cast<const uint4 *>(row) + W0 / 4;
+  unsigned W[CW];
 #pragma unroll
-  for (int q = 0; q < NCH; ++q) {
+  for (int q = 0; q < CW / 4; ++q) {
     const uint4 u = r4[q];
     W[4 * q + 0] = u.x;
     W[4 * q + 1] = u.y;
     W[4 * q + 2] = u.z;
     W[4 * q + 3] = u.w;
   }
-  float a[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-  for (int j = 0; j < Q23<NCH>::NQ; ++j) {
+  for (int j = 0; j < NJ; ++j) {
     const int k = (3 * j) >> 2, o = (3 * j) & 3;
     const unsigned sel = o == 0 ? 0xA210u : o == 1 ? 0xB321u : o == 2 ? 0xC432u : 0xD543u;
     unsigned bits;  // (prmt's sign-replication selector bit is outside __byte_perm's documented range)
-    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(bits) : "r"(W[k]), "r"(W[k + 1 < 4 * NCH ? k + 1 : k]), "r"(sel));
-    a[j & 3] = fmaf(w[j], __uint_as_float(bits), a[j & 3]);
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(bits) : "r"(W[k]), "r"(W[k + 1 < CW ? k + 1 : k]), "r"(sel));
+    a[(J0 + j) & 3] = fmaf(w[J0 + j], __uint_as_float(bits), a[(J0 + j) & 3]);
+  }
+}
+
+template <int NCH>
+__device__ __forceinline__ float screen_row_q23(const float *row, const float (&w)[Q23<NCH>::NQ]) {
+  constexpr int NQ = Q23<NCH>::NQ;
+  float a[4] = {0.f, 0.f, 0.f, 0.f};
+  if constexpr (NCH <= 4) {
+    q23_group<0, 4 * NCH, 0, NQ, NQ>(row, w, a);  // the whole row's words in registers
+  } else {
+    // wide rows: 48-byte groups of 16 entries (12 words live at a time), then the rest
+    static_assert(NCH == 10, "wide q23 rows are built for 10 chunks (d <= 53)");
+    q23_group<0, 12, 0, 16, NQ>(row, w, a);
+    q23_group<12, 12, 16, 16, NQ>(row, w, a);
+    q23_group<24, 12, 32, 16, NQ>(row, w, a);
+    q23_group<36, 4, 48, NQ - 48, NQ>(row, w, a);
   }
   return (a[0] + a[1]) + (a[2] + a[3]);
 }
@@ -1798,6 +1815,8 @@ static int dispatch_block(const Plan &P, const JoinParams &p, const int32_t *ali
       return launch_join<G, 2, 1, GTAB, SCR_Q23>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st);
     if (p.nvq == 3)
       return launch_join<G, 3, 1, GTAB, SCR_Q23>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st);
+    if (p.nvq == 10)
+      return launch_join<G, 10, 1, GTAB, SCR_Q23>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st);
     return launch_join<G, 4, 1, GTAB, SCR_Q23>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st);
   }
 #define KNND_CALL(NV)                                                                                          \
@@ -1813,6 +1832,7 @@ static int dispatch_warp(const Plan &P, const JoinParams &p, const int32_t *alis
     if (p.nvq == 1) return launch_warp<1, 1, SCR_Q23>(p, alist, acount, logH, SW, cap, st);
     if (p.nvq == 2) return launch_warp<2, 1, SCR_Q23>(p, alist, acount, logH, SW, cap, st);
     if (p.nvq == 3) return launch_warp<3, 1, SCR_Q23>(p, alist, acount, logH, SW, cap, st);
+    if (p.nvq == 10) return launch_warp<10, 1, SCR_Q23>(p, alist, acount, logH, SW, cap, st);
     return launch_warp<4, 1, SCR_Q23>(p, alist, acount, logH, SW, cap, st);
   }
 #define KNND_CALL(NV)                                                             \
@@ -2043,8 +2063,9 @@ int knnd_local_join_peers(const double *points, const float *log32, const double
   p.pstride = d;
   p.aside32 = nullptr;
   if (qrows) {  // the 23-bit fixed-point screen (knnd_kl_q23_prepare)
-    KNND_CHECK_ARG(q_h && (q_ld == 16 || q_ld == 32 || q_ld == 48 || q_ld == 64) && q_ld >= 3 * d && k <= 32,
-                   "knnd_local_join: the q23 screen needs q_h, rows of 16, 32, 48 or 64 bytes (>= 3 d) and K <= 32 "
+    KNND_CHECK_ARG(q_h && (q_ld == 16 || q_ld == 32 || q_ld == 48 || q_ld == 64 || q_ld == 160) && q_ld >= 3 * d &&
+                       k <= 32,
+                   "knnd_local_join: the q23 screen needs q_h, rows of 16, 32, 48, 64 or 160 bytes (>= 3 d) and K <= 32 "
                    "(q_ld=%d d=%d K=%d)",
                    q_ld, d, k);
     p.log32 = reinterpret_cast<const float *>(qrows);

@@ -106,7 +106,14 @@ def upload(host: np.ndarray, device: torch.device) -> torch.Tensor:
     return out
 
 
-Q23_MAX_ROW_BYTES = 64  # the join's Q23 screen is built for rows of 16 / 32 / 48 / 64 bytes (d <= 5 / 10 / 16 / 21)
+def q23_row_bytes(d: int) -> int:
+    """Row size of the join's Q23 screen for dimension d (3 bytes per entry), or 0
+    where the kernels have no such row: 16 / 32 / 48 / 64 bytes for d <= 5 / 10 /
+    16 / 21, and 160 bytes for d = 43..53 (where the fp32 rows take 176-212)."""
+    need = 3 * d
+    if need <= 64:
+        return (need + 15) // 16 * 16
+    return 160 if 128 < need <= 160 else 0
 
 
 def _dev(device) -> torch.device:
@@ -141,14 +148,14 @@ class DeviceTables:
                   self.log64.data_ptr(), self.xlogx.data_ptr(), _stream(device))
         self.dplan = self.d  # the screen row width the join plans for
         # The join's 23-bit fixed-point screen (knnd_kl_q23_prepare): 3 bytes per entry,
-        # rows of 16 to 64 bytes — at d = 20 two aligned sectors in one 128-byte
+        # rows of 16 to 64 bytes (160 at d = 43..53) — at d = 20 two aligned sectors in one 128-byte
         # line per row instead of three sectors over 1.5 lines.  The random row gather
         # sets the join's rate (tools/row_probe.cu), the error bound is as tight as
         # the fp32 screen's, and results do not depend on it (KNND_Q23=0 keeps the
         # fp32 rows).  Not built when a log is not finite (a zero coordinate).
         self.q23 = self.qh23 = None
-        self.q23_bytes = (3 * self.d + 15) // 16 * 16
-        if os.environ.get("KNND_Q23", "1") != "0" and self.q23_bytes <= Q23_MAX_ROW_BYTES:
+        self.q23_bytes = q23_row_bytes(self.d)
+        if os.environ.get("KNND_Q23", "1") != "0" and self.q23_bytes:
             self.q23 = torch.empty((self.n, self.q23_bytes), dtype=torch.uint8, device=device)
             self.qh23 = torch.empty(self.q23_bytes // 3, dtype=torch.float32, device=device)
             ws = torch.empty(max(int(_lib.load().knnd_kl_q23_workspace_bytes(self.d)), 256), dtype=torch.uint8,

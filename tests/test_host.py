@@ -261,3 +261,11 @@ def test_fused_exchange_states_never_alias_a_reused_table(small_meta):
     for st in seen[:-2]:  # tables overwritten two rounds later
         with pytest.raises(RuntimeError, match="reused by a later round"):
             st.friends
+
+
+def test_q23_row_sizes():
+    """3 bytes per entry in the smallest row the kernels have; none where it would not pay."""
+    from paper_2202_00517_b200.similarity import q23_row_bytes
+
+    assert [q23_row_bytes(d) for d in (1, 5, 6, 10, 11, 16, 17, 20, 21)] == [16, 16, 32, 32, 48, 48, 64, 64, 64]
+    assert [q23_row_bytes(d) for d in (22, 42, 43, 50, 53, 54, 96)] == [0, 0, 160, 160, 160, 0, 0]

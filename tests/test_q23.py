@@ -60,10 +60,12 @@ def test_q23_non_finite_logs_keep_fp32(cuda, q23_on):
     assert tabs.q23 is None
 
 
-@pytest.mark.parametrize("name", ["n1000_d20_k20_s1", "n1500_d16_k10_s7", "n800_d10_k40_s5"])
+@pytest.mark.parametrize("name", ["n1000_d20_k20_s1", "n1500_d16_k10_s7", "n800_d10_k40_s5", "n600_d50_k30_s2",
+                                  "n4000_d5_k10_s0"])
 def test_q23_small_trajectories(cuda, screen, small_meta, name):
     """Full descents with the q23 screen reproduce the reference's per-round
-    tables (d = 20, 16, 10: rows of 64 / 48 / 32 bytes; K = 40 > 32 takes the fp32 screen)."""
+    tables (d = 20, 16, 10, 50, 5: rows of 64 / 48 / 32 / 160 / 16 bytes; K = 40 > 32 takes
+    the fp32 screen)."""
     meta = small_meta[name]
     n, d, k, seed = meta["n"], meta["d"], meta["k"], meta["seed"]
     pts = port.experiment_points(n, d, seed)

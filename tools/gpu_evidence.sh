@@ -1,6 +1,7 @@
 # Round evidence (one call): all GPU tests + smoke + the bench lines (C3 both arms,
-# C2/C4/C5), the launch list of one C3 step, ncu --set full captures of the W1,
-# B128 (2^12) and B256 join launches and of the tensor-core exact K-NN.
+# C2/C4/C5), the launch list of one C3 step and the ncu --set full capture of one W1
+# join launch (the block-class / C5 / exact K-NN captures: tools/gpu_ncu_blocks.sh,
+# summarised on the box — gpurun_out holds 64 MiB).
 bash tools/gpu_full.sh
 for c in c2 c4 c5; do
   timeout 900 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$c.log 2>&1
@@ -11,12 +12,5 @@ $B > gpurun_out/bench_short.log 2>&1 && \
 KNND_CLASS_TIMING=1 $B > gpurun_out/bench_short_ct.log 2>&1 && \
   KNND_CLASS_TIMING=1 ncu --set full --clock-control none --import-source on -k regex:join_warp_kernel -s 9 -c 1 \
     -o gpurun_out/bench_w1 $B > gpurun_out/ncu_bench_full.log 2>&1
-KNND_CLASS_TIMING=1 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k "regex:join_kernel<128" -s 9 -c 1 -o gpurun_out/bench_b128 $B > gpurun_out/ncu_bench_b128.log 2>&1
-KNND_CLASS_TIMING=1 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k "regex:join_kernel<256" -s 4 -c 1 -o gpurun_out/bench_b256 $B > gpurun_out/ncu_bench_b256.log 2>&1
-python tools/exact_probe.py 1000000 20 20 100000 > gpurun_out/exact_plain.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:exact_tc -s 1 -c 1 -o gpurun_out/exact_tc \
-    python tools/exact_probe.py 1000000 20 20 100000 > gpurun_out/ncu_exact.log 2>&1
 timeout 300 python tools/exact_probe.py 1000000 20 20 all > gpurun_out/exact_full.log 2>&1
 tail -2 gpurun_out/pytest_gpu.log; tail -1 gpurun_out/smoke.log; ls gpurun_out

@@ -9,7 +9,7 @@ summ() {  # report label
 }
 KNND_CLASS_TIMING=1 $B > gpurun_out/bench_short_ct.log 2>&1 && \
 KNND_CLASS_TIMING=1 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k 'regex:join_kernel<\(int\)128, \(int\)5, \(int\)1, \(bool\)0, \(bool\)0' -s 9 -c 1 -o gpurun_out/bench_b128 $B > gpurun_out/ncu_bench_b128.log 2>&1
+    -k 'regex:join_kernel<\(int\)128, \(int\)4, \(int\)1, \(bool\)0, \(bool\)0' -s 9 -c 1 -o gpurun_out/bench_b128 $B > gpurun_out/ncu_bench_b128.log 2>&1
 summ bench_b128 "B128 (2^12 table) join launch, C3 bench step"
 KNND_CLASS_TIMING=1 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
     -k 'regex:join_kernel<\(int\)256' -s 4 -c 1 -o gpurun_out/bench_b256 $B > gpurun_out/ncu_bench_b256.log 2>&1

@@ -77,6 +77,17 @@ int main(int argc, char **argv) {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   const int blocks_per_sm = argc > 3 ? atoi(argv[3]) : 4;
+  {  // argv[4]: cudaLimitMaxL2FetchGranularity (bytes; a hint the platform may clamp)
+    size_t g0 = 0, g1 = 0;
+    cudaDeviceGetLimit(&g0, cudaLimitMaxL2FetchGranularity);
+    if (argc > 4) {
+      cudaError_t e = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(argv[4]));
+      cudaDeviceGetLimit(&g1, cudaLimitMaxL2FetchGranularity);
+      printf("L2 fetch granularity: default %zu, asked %s -> %zu (%s)\n", g0, argv[4], g1, cudaGetErrorString(e));
+    } else {
+      printf("L2 fetch granularity: %zu\n", g0);
+    }
+  }
   const int grid = sms * blocks_per_sm;
   const long nw = (long)grid * WARPS;
   float *tab, *out;
