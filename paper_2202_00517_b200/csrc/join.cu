@@ -567,7 +567,7 @@ constexpr int LSTAGE_FLOATS = 1536;  // per-warp staging (6 KB, two buffers) in 
 // per-warp staging floats of the global-table class: 6 KB, and at least 2 x 8 rows
 __host__ __device__ inline int lstage_floats(int ld) { return LSTAGE_FLOATS > 16 * ld ? LSTAGE_FLOATS : 16 * ld; }
 
-__host__ __device__ inline SmemLayout smem_layout(int G, bool gtab, int d, int ld, int H, int SW) {
+__host__ __device__ inline SmemLayout smem_layout(int G, bool gtab, int d, int ld, int H, int SW, int XT = 0) {
   SmemLayout L;
   size_t o = 64;  // header ints: [0] |U| [1] |R| [2] b1 [3] before1 [4] b2, [8..12] next anchor
   L.x32 = o;
@@ -590,7 +590,7 @@ __host__ __device__ inline SmemLayout smem_layout(int G, bool gtab, int d, int l
   if (!gtab) {
     L.stage = 0;  // staging uses the (dead) table
     L.table = o;
-    o = al16(o + (size_t)H * 4);
+    o = al16(o + (size_t)(H + XT) * 4);  // XT: extra staging ints past the hash table (launch_join)
     L.list = o;
     o = al16(o + (size_t)(H / 2) * 4);
   } else {
@@ -641,14 +641,14 @@ __device__ __forceinline__ void hist_find(const int *hist, int target, int *hdr,
 template <int G, int NV4, int KPL, bool GTAB, bool PF, int SCR>
 __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__restrict__ alist,
                                                  const int32_t *__restrict__ acount, int logH, int SW,
-                                                 int32_t *__restrict__ gslab, int64_t slab_ints) {
+                                                 int32_t *__restrict__ gslab, int64_t slab_ints, int XT) {
   constexpr int W = G / 32;
   constexpr bool Q23S = SCR == SCR_Q23;
   extern __shared__ __align__(16) unsigned char sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int H = 1 << logH;
   const unsigned shift = 32u - (unsigned)logH;
-  const SmemLayout L = smem_layout(G, GTAB, p.d, p.ld, H, SW);
+  const SmemLayout L = smem_layout(G, GTAB, p.d, p.ld, H, SW, XT);
   int *hdr = reinterpret_cast<int *>(sm);
   float *red = reinterpret_cast<float *>(sm + L.red);
   int *hist = reinterpret_cast<int *>(sm + L.hist);
@@ -899,10 +899,10 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
       // staging: the table past the scores ([0, U), U <= H/2), split over warps,
       // two buffers per warp
       const int u4 = (U + 3) & ~3;
-      const int per_warp_floats = ((H - u4) / W) & ~3;
+      const int per_warp_floats = ((H + XT - u4) / W) & ~3;
       wrows = min(32, per_warp_floats / (2 * ld));
       wstage = reinterpret_cast<float *>(table + u4) + (size_t)warp * per_warp_floats;
-      KNND_DCHECK(U == 0 || (wrows >= 1 && u4 + (size_t)(warp + 1) * per_warp_floats <= (size_t)H &&
+      KNND_DCHECK(U == 0 || (wrows >= 1 && u4 + (size_t)(warp + 1) * per_warp_floats <= (size_t)(H + XT) &&
                              2 * wrows * ld <= per_warp_floats));
     }
     float mn = __int_as_float(0x7f800000), mx = -mn, am = 0.f;
@@ -1747,7 +1747,7 @@ static int launch_join(const JoinParams &p, const int32_t *alist, const int32_t 
   auto kern = (!GTAB && logH >= 13) ? join_kernel<G, NV4, KPL, GTAB, !GTAB, SCR>
                                     : join_kernel<G, NV4, KPL, GTAB, false, SCR>;
   const SmemLayout L = smem_layout(G, GTAB, p.d, p.ld, 1 << logH, SW);
-  const size_t smem = L.total;
+  size_t smem = L.total;
   if (smem > 227 * 1024) {
     set_error("local join: shared memory %zu exceeds 227 KB (d=%d, H=%d)", smem, p.d, 1 << logH);
     return KNND_EUNSUPPORTED;
@@ -1758,9 +1758,35 @@ static int launch_join(const JoinParams &p, const int32_t *alist, const int32_t 
     set_error("local join: kernel cannot be resident (smem=%zu)", smem);
     return KNND_EUNSUPPORTED;
   }
+  // The staging rows of the screen live in the table past the scores: when that
+  // leaves a warp fewer than 32 rows per buffer (the 2^12 class: 18), the shared
+  // memory the resident blocks leave unused extends the table — the per-batch
+  // instructions are amortised over more rows (the block classes are issue-bound).
+  int XT = 0;
+  if constexpr (!GTAB) {
+    const int H = 1 << logH;
+    const int srow = 2 * (SCR == SCR_Q23 ? (NV4 | 1) * 4 : p.ld);  // floats per staged row, two buffers
+    const int have = (H / 2) / (G / 32) / srow;                    // rows per buffer at the largest |U| = H / 2
+    if (have < 32) {
+      // (a block's allocation is rounded up to 1 KB, plus 1 KB the system reserves per block)
+      const size_t cap_b = (((size_t)228 * 1024 / per_sm - 1024) >> 10) << 10;
+      const size_t spare = cap_b > smem ? cap_b - smem : 0;
+      const size_t want = (size_t)(32 - have) * srow * (G / 32) * 4;
+      const size_t extra = spare < want ? spare : want;
+      int per_sm2 = 0;
+      if (extra >= 1024 && smem + extra <= 227 * 1024 &&
+          kernel_occupancy((const void *)kern, G, smem + extra, &per_sm2) == KNND_OK && per_sm2 == per_sm) {
+        XT = (int)(extra / 4);
+        smem += extra;
+      }
+    }
+  }
   int grid = per_sm * num_sms();
   if (grid_cap > 0 && grid > grid_cap) grid = grid_cap;
-  kern<<<grid, G, smem, st>>>(p, alist, acount, logH, SW, gslab, slab_ints);
+  if (getenv("KNND_CLASS_TIMING"))
+    fprintf(stderr, "knnd block class G=%d logH=%d: %d blocks/SM, smem %zu B (%d extra staging ints)\n", G, logH, per_sm,
+            smem, XT);
+  kern<<<grid, G, smem, st>>>(p, alist, acount, logH, SW, gslab, slab_ints, XT);
   KNND_LAUNCHED(1);
   return KNND_OK;
 }
