@@ -392,11 +392,15 @@ def b200_arm(args):
     # ---- roofline of the local join (per rank: this rank's comparisons / its launch time)
     peak, peak_src = peaks()
     bytes_per_cmp = 4 * d
+    gathered = int(tabs.q23_bytes) if getattr(tabs, "q23", None) is not None and k <= 32 else int(tabs.ld) * 4
     achieved = bytes_per_cmp * join_comps / (join_ms / 1e3) / 1e9 if join_ms > 0 else 0.0
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": ncu_traffic(args.config)[0], "traffic_launch": ncu_traffic(args.config)[1],
             "kernel": "knnd_local_join (classify + size-class join launches)",
             "bytes_per_comparison": bytes_per_cmp, "peak_source": peak_src,
+            # what the screen actually gathers per comparison: the Q23 row (3 bytes per
+            # entry, 16-byte multiples) where the tables have one, else the fp32 row
+            "gathered_bytes_per_comparison": gathered, "achieved_gathered": achieved * gathered / bytes_per_cmp,
             "comparisons_per_s": join_comps / (join_ms / 1e3) if join_ms > 0 else 0.0,
             "share_of_step": join_ms / sum(step_ms) if step_ms else None}
 
