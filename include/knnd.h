@@ -272,7 +272,11 @@ int knnd_l2_local_join(const float *anchor32, const float *cand32, const double 
                        int32_t *out_ids, double *out_d2, int32_t *out_ucount,
                        unsigned long long *tally, const float *bound_in, float *bound_out, void *ws,
                        size_t ws_bytes, void *stream);
-/* knnd_l2_local_join with the fused table exchange (and side stream) of knnd_local_join_peers */
+/* knnd_l2_local_join with the fused table exchange (and side stream) of knnd_local_join_peers.
+ * qrows / q_h / q_ld (nullable qrows): the 23-bit fixed-point screen rows, as for the KL join —
+ * knnd_kl_q23_prepare run on the n x (d + 1) fp64 table of the cand32 columns (v - mu, |v - mu|^2),
+ * q_ld = 32, 48 or 64 >= 3 (d + 1), K <= 32.  The weights 2 (x - mu)_j h_j 2^126 must stay inside fp32's normal
+ * range (the caller checks the data's scale). */
 int knnd_l2_local_join_peers(const float *anchor32, const float *cand32, const double *rows64,
                              const double *sq64, int64_t n, int32_t d, int32_t ld32,
                              double maxnorm, const int32_t *friends, int32_t k,
@@ -280,8 +284,8 @@ int knnd_l2_local_join_peers(const float *anchor32, const float *cand32, const d
                              int64_t row_hi, int32_t max_indeg, int32_t *out_ids, double *out_d2,
                              int32_t *out_ucount, unsigned long long *tally,
                              const float *bound_in, float *bound_out, void *ws, size_t ws_bytes,
-                             int32_t *const *peer_tables, int32_t npeers, void *stream,
-                             void *side_stream);
+                             int32_t *const *peer_tables, int32_t npeers, const void *qrows,
+                             const float *q_h, int32_t q_ld, void *stream, void *side_stream);
 int knnd_l2_exact_knn(const float *anchor32, const float *cand32, const double *rows64,
                       const double *sq64, int64_t n, int32_t d, int32_t ld32, double maxnorm,
                       const int32_t *queries, int64_t nq, int32_t k, int32_t cap, int32_t *out_ids,

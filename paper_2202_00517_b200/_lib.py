@@ -53,7 +53,7 @@ _SIGS = {
     "knnd_l2_local_join": ([_P, _P, _P, _P, _I64, _I32, _I32, C.c_double, _P, _I32, _P, _P, _I64, _I64, _I32, _P, _P,
                             _P, _P, _P, _P, _P, _SZ, _P], C.c_int),
     "knnd_l2_local_join_peers": ([_P, _P, _P, _P, _I64, _I32, _I32, C.c_double, _P, _I32, _P, _P, _I64, _I64, _I32,
-                                  _P, _P, _P, _P, _P, _P, _P, _SZ, _P, _I32, _P, _P], C.c_int),
+                                  _P, _P, _P, _P, _P, _P, _P, _SZ, _P, _I32, _P, _P, _I32, _P, _P], C.c_int),
     "knnd_l2_exact_knn": ([_P, _P, _P, _P, _I64, _I32, _I32, C.c_double, _P, _I64, _I32, _I32, _P, _P, _P, _P, _SZ,
                            _P], C.c_int),
     "knnd_random_kout_workspace_bytes": ([_I64, _I32], _SZ),

@@ -42,6 +42,8 @@ constexpr int EMPTY = -1;
 // the screen's row format (template parameter SCR of the join kernels)
 constexpr int SCR_F32 = 0;  // fp32 log rows
 constexpr int SCR_Q23 = 1;  // 23-bit fixed point in 3 bytes per entry (knnd_kl_q23_prepare)
+constexpr int SCR_Q23L2 = 2;  // the same rows for the Euclidean scorer (signed weights: its own instantiations,
+                              // so the KL kernels carry none of its branches — they had cost W1 0.8%)
 constexpr int UNR1 = 4;  // pre-dedup ids loaded per thread before inserting
 
 struct JoinParams {
@@ -366,6 +368,26 @@ __device__ __forceinline__ float q23_weights(const double *x64, const float *__r
   return s * 0x1p-75f * (1.f + 0x1p-9f) + 1e-36f;  // sum_j w_j 2^-150 = 2^-23 A1 / 2
 }
 
+// The Euclidean scorer's weights, from its anchor-side fp32 row xs32 = (2 (x - mu), -1)
+// over dq = d + 1 columns.  They are signed, so the relative part of the bound cannot
+// use a candidate's own value: abq = sum_j |w_j| F_max bounds sum_j |w_j F_j| of every
+// candidate (2^-23 sum_j |a_j| range_j).  (A separate function: selecting the source
+// per entry inside q23_weights cost the KL kernels 6%.)
+template <int NCH>
+__device__ __forceinline__ float q23_weights_signed(const float *xs32, const float *__restrict__ qh, int dq,
+                                                    float (&w)[Q23<NCH>::NQ], float &abq) {
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < Q23<NCH>::NQ; ++j) {
+    const float x = j < dq ? xs32[j] : 0.f;
+    const float h = j < dq ? __ldg(qh + j) : 0.f;
+    w[j] = (x * h) * 0x1p126f;
+    s = fmaf(fabsf(w[j]), 0x1p-75f, s);
+  }
+  abq = s * 0x1p-51f * (1.f + 0x1p-9f);            // sum_j |w_j| 2^-126
+  return s * 0x1p-75f * (1.f + 0x1p-9f) + 1e-36f;  // sum_j |w_j| 2^-150 = 2^-23 A1 / 2
+}
+
 // entries [J0, J0 + NJ) of a row from the CW words at word offset W0 (48 bytes
 // hold 16 entries exactly, so 3-chunk groups are self-contained)
 template <int W0, int CW, int J0, int NJ, int NQ>
@@ -643,7 +665,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
                                                  const int32_t *__restrict__ acount, int logH, int SW,
                                                  int32_t *__restrict__ gslab, int64_t slab_ints, int XT) {
   constexpr int W = G / 32;
-  constexpr bool Q23S = SCR == SCR_Q23;
+  constexpr bool Q23S = SCR != SCR_F32, Q23SIGNED = SCR == SCR_Q23L2;
   extern __shared__ __align__(16) unsigned char sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int H = 1 << logH;
@@ -712,7 +734,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     for (int i = tid; i < d; i += G) cp_async8(x64 + i, p.points + (int64_t)xp * p.pstride + i);
     if (p.aside32)
 #pragma unroll 1
-      for (int i = tid; i < ld / 4; i += G) cp_async16(x32 + 4 * i, p.aside32 + (int64_t)xp * ld + 4 * i);
+      for (int i = tid; i < p.ld / 4; i += G) cp_async16(x32 + 4 * i, p.aside32 + (int64_t)xp * p.ld + 4 * i);
     cp_async_commit();
   };
   if (tid == 0) {
@@ -906,12 +928,16 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
                              2 * wrows * ld <= per_warp_floats));
     }
     float mn = __int_as_float(0x7f800000), mx = -mn, am = 0.f;
-    float slack = p.slack;
+    float slack = p.slack, abq = 0.f;  // (abq: Q23, Euclidean — the bound on every candidate's sum |w F|)
     float best0 = mn, best1 = mn;  // this lane's two smallest screened values
     float4 xreg[NV4 > 0 && !Q23S ? NV4 : 1];  // the anchor's fp32 row in registers
     float wq[Q23<Q23S ? NV4 : 1>::NQ];  // Q23: the anchor's weights
     if constexpr (Q23S) {
-      slack = q23_weights<NV4>(x64, p.qh, d, wq);  // the quantisation part of the bound, per anchor
+      // the quantisation part of the bound, per anchor (+ the Euclidean scorer's fp64 term in these units)
+      if constexpr (Q23SIGNED)
+        slack = q23_weights_signed<NV4>(x32, p.qh, p.d64, wq, abq) + p.slack * 0x1p-23f;
+      else
+        slack = q23_weights<NV4>(x64, p.qh, d, wq);
     } else if constexpr (NV4 > 0) {
 #pragma unroll
       for (int q = 0; q < NV4; ++q) xreg[q] = reinterpret_cast<const float4 *>(x32)[q];
@@ -952,7 +978,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
         float ce, ab;
         if constexpr (Q23S) {
           ce = screen_row_q23<NV4>(wstage + buf * wrows * ld + rl * ld, wq);
-          ab = ce;  // every term is >= 0
+          ab = ce;  // KL: every term is >= 0 (the Euclidean scorer replaces the maximum by abq below)
         } else if constexpr (NV4 > 0) {
           screen_row_reg<NV4>(wstage + buf * wrows * ld + rl * ld, xreg, p.nonpos, ce, ab);
         } else {
@@ -970,6 +996,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
         __syncwarp();
       }
     }
+    if constexpr (Q23SIGNED) am = abq;  // signed weights: the bound on every candidate's sum |w F|
     if (tid == 0) {  // publish the next anchor (read after the threshold section's barrier)
       hdr[8] = an;
       hdr[9] = xn;
@@ -1082,7 +1109,8 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     // own sum |x log y| (+ slack), which equals its screened value (<= theta)
     // when every term has one sign — usually several times tighter than the
     // bound over all of U, so fewer rows fall back to the fp64 ranking
-    const float ebase_r = (Q23S || p.nonpos) ? p.band * fminf(am, theta) + slack : ebase;
+    const float ebase_r =
+        (!Q23SIGNED && (Q23S || (p.metric == METRIC_KL && p.nonpos))) ? p.band * fminf(am, theta) + slack : ebase;
     if (hdr[8] < count) prefetch(pb ^ 1, hdr[9], hdr64[0], hdr[12]);
 
     // ---- phase 3: collect every candidate the screen cannot exclude
@@ -1178,7 +1206,7 @@ __global__ void __launch_bounds__(128, 4)
     join_warp_kernel(JoinParams p, const int32_t *__restrict__ alist, const int32_t *__restrict__ acount, int logH,
                      int SW, int cap) {
   constexpr int Q = 2 * KPL;  // per-lane kept screened values
-  constexpr bool Q23S = SCR == SCR_Q23;
+  constexpr bool Q23S = SCR != SCR_F32, Q23SIGNED = SCR == SCR_Q23L2;
   extern __shared__ __align__(16) unsigned char sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int H = 1 << logH;
@@ -1263,9 +1291,13 @@ __global__ void __launch_bounds__(128, 4)
     __syncwarp();
     float4 xreg[NV4 > 0 && !Q23S ? NV4 : 1];  // the anchor's fp32 row in registers
     float wq[Q23<Q23S ? NV4 : 1>::NQ];  // Q23: the anchor's weights
-    float slack = p.slack;                      // the absolute part of the fp32 / Q23 bound
+    float slack = p.slack, abq = 0.f;           // the absolute part of the fp32 / Q23 bound (abq: Euclidean Q23)
     if constexpr (Q23S) {
-      slack = q23_weights<NV4>(x64, p.qh, d, wq);  // the quantisation part of the bound, per anchor
+      // the quantisation part of the bound, per anchor (+ the Euclidean scorer's fp64 term in these units)
+      if constexpr (Q23SIGNED)
+        slack = q23_weights_signed<NV4>(x32, p.qh, p.d64, wq, abq) + p.slack * 0x1p-23f;
+      else
+        slack = q23_weights<NV4>(x64, p.qh, d, wq);
     } else if constexpr (NV4 > 0) {
 #pragma unroll
       for (int q = 0; q < NV4; ++q) xreg[q] = reinterpret_cast<const float4 *>(x32)[q];
@@ -1428,7 +1460,7 @@ __global__ void __launch_bounds__(128, 4)
         float ce, ab;
         if constexpr (Q23S) {
           ce = screen_row_q23<NV4>(stage + buf * rows * ld + rl * ld, wq);
-          ab = ce;  // every term is >= 0
+          ab = ce;  // KL: every term is >= 0 (the Euclidean scorer replaces the maximum by abq below)
         } else if constexpr (NV4 > 0) {
           screen_row_reg<NV4>(stage + buf * rows * ld + rl * ld, xreg, p.nonpos, ce, ab);
         } else {
@@ -1453,6 +1485,7 @@ __global__ void __launch_bounds__(128, 4)
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) am = fmaxf(am, __shfl_xor_sync(FULL, am, o));
+    if constexpr (Q23SIGNED) am = abq;  // signed weights: the bound on every candidate's sum |w F|
     // Threshold.  The previous round's bound of this row (the largest screened
     // value among the current friends, all of which are in U) is a valid T; it
     // is used when it admits at most 32 candidates, else T comes from the lanes'
@@ -1496,7 +1529,8 @@ __global__ void __launch_bounds__(128, 4)
     // own sum |x log y| (+ slack), which equals its screened value (<= theta)
     // when every term has one sign — usually several times tighter than the
     // bound over all of U, so fewer rows fall back to the fp64 ranking
-    const float ebase_r = (Q23S || p.nonpos) ? p.band * fminf(am, theta) + slack : ebase;
+    const float ebase_r =
+        (!Q23SIGNED && (Q23S || (p.metric == METRIC_KL && p.nonpos))) ? p.band * fminf(am, theta) + slack : ebase;
 
     // ---- phase 3: R (ids and screened values) in place at the front of list / scores
     int nR = 0;
@@ -1765,7 +1799,7 @@ static int launch_join(const JoinParams &p, const int32_t *alist, const int32_t 
   int XT = 0;
   if constexpr (!GTAB) {
     const int H = 1 << logH;
-    const int srow = 2 * (SCR == SCR_Q23 ? (NV4 | 1) * 4 : p.ld);  // floats per staged row, two buffers
+    const int srow = 2 * (SCR != SCR_F32 ? (NV4 | 1) * 4 : p.ld);  // floats per staged row, two buffers
     const int have = (H / 2) / (G / 32) / srow;                    // rows per buffer at the largest |U| = H / 2
     if (have < 32) {
       // (a block's allocation is rounded up to 1 KB, plus 1 KB the system reserves per block)
@@ -1834,6 +1868,13 @@ static int launch_warp(const JoinParams &p, const int32_t *alist, const int32_t 
 template <int G, bool GTAB>
 static int dispatch_block(const Plan &P, const JoinParams &p, const int32_t *alist, const int32_t *acount,
                           int logH, int SW, int32_t *gslab, int64_t slab_ints, int grid_cap, cudaStream_t st) {
+  if (p.scr == SCR_Q23L2) {  // Euclidean: K <= 32, rows of 2 to 4 16-byte chunks; checked at the entry
+    if (p.nvq == 2)
+      return launch_join<G, 2, 1, GTAB, SCR_Q23L2>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st);
+    if (p.nvq == 3)
+      return launch_join<G, 3, 1, GTAB, SCR_Q23L2>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st);
+    return launch_join<G, 4, 1, GTAB, SCR_Q23L2>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st);
+  }
   if (p.scr == SCR_Q23) {  // K <= 32, rows of 1 to 4 16-byte chunks; checked at the entry
     if (p.nvq == 1)
       return launch_join<G, 1, 1, GTAB, SCR_Q23>(p, alist, acount, logH, SW, gslab, slab_ints, grid_cap, st);
@@ -1854,6 +1895,11 @@ static int dispatch_block(const Plan &P, const JoinParams &p, const int32_t *ali
 
 static int dispatch_warp(const Plan &P, const JoinParams &p, const int32_t *alist, const int32_t *acount, int logH,
                          int SW, int cap, cudaStream_t st) {
+  if (p.scr == SCR_Q23L2) {
+    if (p.nvq == 2) return launch_warp<2, 1, SCR_Q23L2>(p, alist, acount, logH, SW, cap, st);
+    if (p.nvq == 3) return launch_warp<3, 1, SCR_Q23L2>(p, alist, acount, logH, SW, cap, st);
+    return launch_warp<4, 1, SCR_Q23L2>(p, alist, acount, logH, SW, cap, st);
+  }
   if (p.scr == SCR_Q23) {
     if (p.nvq == 1) return launch_warp<1, 1, SCR_Q23>(p, alist, acount, logH, SW, cap, st);
     if (p.nvq == 2) return launch_warp<2, 1, SCR_Q23>(p, alist, acount, logH, SW, cap, st);
@@ -1943,7 +1989,7 @@ static int join_run(const char *who, JoinParams &p, int64_t n, int32_t dplan, in
   p.band = (float)((ld32 + 8) * 0x1p-24);
   // Q23: three roundings in a weight (x, h, their product), a chain of ceil(NQ / 4)
   // FMAs and two adds per entry — (1 + u)^(ceil(NQ / 4) + 5) - 1, one more u of margin
-  if (p.scr == SCR_Q23) p.band = (float)((((16 * p.nvq) / 3 + 3) / 4 + 6) * 0x1p-24);
+  if (p.scr != SCR_F32) p.band = (float)((((16 * p.nvq) / 3 + 3) / 4 + 6) * 0x1p-24);
 
   KNND_CUDA(cudaMemsetAsync(counts, 0, 64, st));
   {
@@ -2118,8 +2164,8 @@ int knnd_l2_local_join_peers(const float *anchor32, const float *cand32, const d
                              const int64_t *indptr, const int32_t *indices, int64_t row_lo, int64_t row_hi,
                              int32_t max_indeg, int32_t *out_ids, double *out_d2, int32_t *out_ucount,
                              unsigned long long *tally, const float *bound_in, float *bound_out, void *ws,
-                             size_t ws_bytes, int32_t *const *peer_tables, int32_t npeers, void *stream,
-                             void *side_stream) {
+                             size_t ws_bytes, int32_t *const *peer_tables, int32_t npeers, const void *qrows,
+                             const float *q_h, int32_t q_ld, void *stream, void *side_stream) {
   KNND_CHECK_ARG(anchor32 && cand32 && rows64 && sq64, "knnd_l2_local_join: null pointer");
   JoinParams p{};
   p.points = rows64;  // the anchor's fp64 coordinates: the first d entries of its row
@@ -2143,6 +2189,16 @@ int knnd_l2_local_join_peers(const float *anchor32, const float *cand32, const d
   p.pstride = d + 1;
   p.aside32 = anchor32;
   p.slack = (float)((d + 4) * 0x1p-53 * 4.0 * maxnorm * maxnorm);
+  if (qrows) {  // the 23-bit fixed-point screen over (v - mu, |v - mu|^2) (knnd_kl_q23_prepare on those columns)
+    KNND_CHECK_ARG(q_h && (q_ld == 32 || q_ld == 48 || q_ld == 64) && q_ld >= 3 * (d + 1) && k <= 32,
+                   "knnd_l2_local_join: the q23 screen needs q_h, rows of 32, 48 or 64 bytes (>= 3 (d + 1)) "
+                   "and K <= 32 (q_ld=%d d=%d K=%d)",
+                   q_ld, d, k);
+    p.log32 = reinterpret_cast<const float *>(qrows);
+    p.qh = q_h;
+    p.nvq = q_ld / 16;
+    p.scr = SCR_Q23L2;
+  }
   if (int rc = set_peers(p, "knnd_l2_local_join", peer_tables, npeers)) return rc;
   return join_run("knnd_l2_local_join", p, n, d + 1, k, row_lo, row_hi, max_indeg, ws, ws_bytes, stream,
                   side_stream);
@@ -2156,7 +2212,7 @@ int knnd_l2_local_join(const float *anchor32, const float *cand32, const double 
                        void *stream) {
   return knnd_l2_local_join_peers(anchor32, cand32, rows64, sq64, n, d, ld32, maxnorm, friends, k, indptr, indices,
                                   row_lo, row_hi, max_indeg, out_ids, out_d2, out_ucount, tally, bound_in, bound_out,
-                                  ws, ws_bytes, nullptr, 0, stream, nullptr);
+                                  ws, ws_bytes, nullptr, 0, nullptr, nullptr, 0, stream, nullptr);
 }
 
 }  // extern "C"

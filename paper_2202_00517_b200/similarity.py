@@ -218,16 +218,37 @@ class L2Tables:
         self.maxnorm = float(np.sqrt(max(float(sq.max()), 0.0))) if sq.size else 0.0
         _lib.call("knnd_l2_prepare", v.data_ptr(), sq_d.data_ptr(), self.n, self.d, self.ld, center.data_ptr(),
                   self.cand32.data_ptr(), self.anchor32.data_ptr(), self.rows64.data_ptr(), _stream(device))
-        torch.cuda.current_stream(device).synchronize()  # v and center are temporaries
+        # The join's Q23 screen (DeviceTables): the candidate columns (v - mu, |v - mu|^2) in
+        # 3 bytes per entry — 64-byte rows at d = 20 against 96.  Its fp32 weights
+        # 2 (x - mu)_j h_j 2^126 must stay in the normal range, so data of an extreme
+        # scale keep the fp32 rows; KNND_Q23=0 keeps them too.
+        self.q23 = self.qh23 = None
+        self.q23_bytes = q23_row_bytes(self.d + 1)
+        if os.environ.get("KNND_Q23", "1") != "0" and self.q23_bytes in (32, 48, 64) and self.n >= 1:
+            c = v - center
+            c64 = torch.cat([c, (c * c).sum(dim=1, keepdim=True)], dim=1).contiguous()
+            q23 = torch.empty((self.n, self.q23_bytes), dtype=torch.uint8, device=device)
+            qh23 = torch.empty(self.q23_bytes // 3, dtype=torch.float32, device=device)
+            ws = torch.empty(max(int(_lib.load().knnd_kl_q23_workspace_bytes(self.d + 1)), 256), dtype=torch.uint8,
+                             device=device)
+            _lib.call("knnd_kl_q23_prepare", c64.data_ptr(), self.n, self.d + 1, self.q23_bytes, q23.data_ptr(),
+                      qh23.data_ptr(), ws.data_ptr(), ws.numel(), _stream(device))
+            amax = torch.cat([2.0 * c.abs().amax(dim=0), c.new_ones(1)])  # |anchor32| per column
+            scale = float((amax.to(torch.float32) * qh23[: self.d + 1]).max().item())  # (synchronises)
+            if np.isfinite(scale) and 2.0 ** -100 < scale < 2.0 ** -6:
+                self.q23, self.qh23 = q23, qh23
+        torch.cuda.current_stream(device).synchronize()  # v, center (and c64, ws) are temporaries
 
     def join(self, table, k, csr, max_indeg, out_rows, tally, out_scores, out_ucount, bound_in, bound_out, ws,
              flags, stream, peers=(), side_stream=None):
+        q23 = self.q23 is not None and k <= 32
         _lib.call("knnd_l2_local_join_peers", self.anchor32.data_ptr(), self.cand32.data_ptr(),
                   self.rows64.data_ptr(), self.sq64.data_ptr(), self.n, self.d, self.ld, self.maxnorm,
                   table.data_ptr(), k, csr.indptr.data_ptr(), csr.indices.data_ptr(), csr.lo, csr.hi, max_indeg,
                   out_rows.data_ptr(), _ptr(out_scores), _ptr(out_ucount), tally.data_ptr(), _ptr(bound_in),
-                  _ptr(bound_out), ws.data_ptr(), ws.numel(), _lib.peer_array(peers), len(peers), stream,
-                  side_stream)
+                  _ptr(bound_out), ws.data_ptr(), ws.numel(), _lib.peer_array(peers), len(peers),
+                  _ptr(self.q23) if q23 else None, _ptr(self.qh23) if q23 else None,
+                  self.q23_bytes if q23 else 0, stream, side_stream)
 
     def join_flags(self) -> int:
         return 0

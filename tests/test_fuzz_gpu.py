@@ -27,7 +27,7 @@ def _cases():
         n = int(rng.integers(max(3 * k, 60), 30_000))
         d = int(rng.choice([2, 3, 5, 7, 10, 16, 20, 24, 33, 50, 60]))
         metric = "kl" if i % 3 else "l2"
-        q23 = metric == "kl" and i % 2 == 0 and d <= 21 and k <= 32
+        q23 = i % 2 == 0 and k <= 32  # the Q23 screen rows where the shape has them, else (and odd cases) fp32
         dup = i % 5 == 4
         out.append((i, n, d, k, metric, q23, dup))
     # edge-heavy shapes: tiny K, n barely above K, one- and two-dimensional data
@@ -35,7 +35,7 @@ def _cases():
     for j, (n, d, k, metric, q23, dup) in enumerate([
             (7, 3, 2, "kl", True, False), (40, 1, 3, "kl", True, False), (300, 2, 2, "kl", False, True),
             (2000, 12, 2, "kl", True, True), (5000, 20, 3, "kl", True, True), (65, 5, 64, "kl", False, False),
-            (3000, 1, 4, "l2", False, False), (4000, 2, 2, "l2", False, True), (20000, 9, 64, "l2", False, True),
+            (3000, 1, 4, "l2", True, False), (4000, 2, 2, "l2", True, True), (20000, 9, 64, "l2", False, True),
             (25000, 16, 32, "kl", True, True), (1200, 60, 64, "kl", False, True), (600, 33, 20, "l2", False, False)]):
         out.append((100 + j, n, d, k, metric, q23, dup))
     return out

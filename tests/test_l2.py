@@ -53,9 +53,16 @@ def test_oracle_l2_matches_reference_trajectory(l2_golden, name):
 # GPU
 
 
+@pytest.fixture(params=["q23", "fp32"])
+def screen(request, monkeypatch):
+    """Both screens of the join: the 23-bit fixed-point rows (default where they exist) and the fp32 rows."""
+    monkeypatch.setenv("KNND_Q23", "1" if request.param == "q23" else "0")
+    return request.param
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", sorted(CASES))
-def test_gpu_l2_trajectory_matches_reference(cuda, l2_golden, name):
+def test_gpu_l2_trajectory_matches_reference(cuda, l2_golden, name, screen):
     import paper_2202_00517_b200 as b2
 
     g = l2_golden[name]
@@ -79,11 +86,12 @@ def test_gpu_l2_trajectory_matches_reference(cuda, l2_golden, name):
 
 
 @pytest.mark.gpu
-def test_gpu_l2_batch_scores_and_join_vs_oracle(cuda):
+def test_gpu_l2_batch_scores_and_join_vs_oracle(cuda, screen):
     import paper_2202_00517_b200 as b2
 
     v = vectors(4000, 12, 21, "normal") * 3.0 + 5.0
     rs = b2.EuclideanRankingSystem(v)
+    assert (rs.device_tables().q23 is not None) == (screen == "q23")
     tab = native.L2Tables(v)
     full = rs.batch_scores(17)
     d2 = np.maximum(tab.xlogx[17] + tab.xlogx - 2.0 * (v @ v[17]), 0.0)
@@ -118,3 +126,23 @@ def test_gpu_l2_accepts_reference_style_system(cuda):
     a, _ = b2.run(b2.Dataset(v), EuclideanRankingSystem(v), b2.DescentConfig(k=8, seed=1))
     b, _ = b2.run(b2.Dataset(v), b2.EuclideanRankingSystem(v), b2.DescentConfig(k=8, seed=1))
     assert np.array_equal(a, b)
+
+
+@pytest.mark.gpu
+def test_gpu_l2_extreme_scales_keep_fp32_rows(cuda):
+    """The Q23 weights 2 (x - mu) h 2^126 must stay in fp32's normal range: data of an
+    extreme scale screen the fp32 rows, and the tables still equal the oracle's."""
+    import paper_2202_00517_b200 as b2
+
+    base = vectors(1500, 10, 3, "normal")
+    for scale, q23 in ((1.0, True), (1e6, False), (1e-40, False)):
+        v = base * scale
+        rs = b2.EuclideanRankingSystem(v)
+        assert (rs.device_tables().q23 is not None) == q23, scale
+        k = 10
+        tab = native.L2Tables(v)
+        init = native.sort_rows(tab, port.random_kout_draws(1500, k, port.substream(2, port.TAG_INIT)))
+        nxt, s = b2.run_round(b2.KnnState(init), rs, b2.DescentConfig(k=k, seed=2))
+        rows, _, _, comps, changed = native.local_join(tab, init)
+        assert np.array_equal(nxt.friends, rows), scale
+        assert (s.comparisons, s.changed_friend_sets) == (comps, changed)

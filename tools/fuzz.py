@@ -21,7 +21,7 @@ for i in range(count):
     n = int(rng.integers(k + 2, int(rng.choice([200, 5000, 60000, 200000]))))
     d = int(rng.integers(1, 70))
     metric = "kl" if rng.random() < 0.7 else "l2"
-    q23 = metric == "kl" and rng.random() < 0.6
+    q23 = rng.random() < 0.6  # the Q23 screen rows where the shape has them (else the fp32 rows)
     dup = rng.random() < 0.3
     os.environ["KNND_Q23"] = "1" if q23 else "0"
     r = np.random.default_rng(seed0 * 1000 + i)
