@@ -91,6 +91,13 @@ size_t knnd_csr_workspace_bytes(int64_t n, int32_t k, int64_t row_lo, int64_t ro
 int knnd_csr_build(const int32_t *friends, int64_t n, int32_t k, int64_t row_lo,
                    int64_t row_hi, int64_t *indptr, int32_t *indices, int32_t *max_indeg,
                    void *ws, size_t ws_bytes, void *stream);
+/* knnd_csr_build that also records counted_event (a cudaEvent_t of the stream's device, nullable)
+ * on the stream once *max_indeg is final — after the counting pass, before the scan and the
+ * fill: the round driver reads its per-round statistics (descent.py:305-313) behind that event
+ * while the rest of the build runs. */
+int knnd_csr_build_ev(const int32_t *friends, int64_t n, int32_t k, int64_t row_lo, int64_t row_hi,
+                      int64_t *indptr, int32_t *indices, int32_t *max_indeg, void *ws,
+                      size_t ws_bytes, void *stream, void *counted_event);
 
 /*
  * The local join for anchors x in [row_lo, row_hi) — _propose_scored

@@ -35,6 +35,7 @@ _SIGS = {
     "knnd_batch_scores": ([_P, _P, _P, _I64, _I32, _I64, _P, _I64, _P, _P], C.c_int),
     "knnd_csr_workspace_bytes": ([_I64, _I32, _I64, _I64], _SZ),
     "knnd_csr_build": ([_P, _I64, _I32, _I64, _I64, _P, _P, _P, _P, _SZ, _P], C.c_int),
+    "knnd_csr_build_ev": ([_P, _I64, _I32, _I64, _I64, _P, _P, _P, _P, _SZ, _P, _P], C.c_int),
     "knnd_local_join_workspace_bytes": ([_I64, _I32, _I32, _I64, _I64, _I32], _SZ),
     "knnd_local_join": ([_P, _P, _P, _P, _I64, _I32, _I32, _P, _I32, _P, _P, _I64, _I64, _I32, _P, _P, _P, _P,
                          _P, _P, _P, _SZ, C.c_uint32, _P], C.c_int),

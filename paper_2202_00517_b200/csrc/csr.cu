@@ -175,6 +175,12 @@ size_t knnd_csr_workspace_bytes(int64_t n, int32_t k, int64_t row_lo, int64_t ro
 
 int knnd_csr_build(const int32_t *friends, int64_t n, int32_t k, int64_t row_lo, int64_t row_hi, int64_t *indptr,
                    int32_t *indices, int32_t *max_indeg, void *ws, size_t ws_bytes, void *stream) {
+  return knnd_csr_build_ev(friends, n, k, row_lo, row_hi, indptr, indices, max_indeg, ws, ws_bytes, stream, nullptr);
+}
+
+int knnd_csr_build_ev(const int32_t *friends, int64_t n, int32_t k, int64_t row_lo, int64_t row_hi, int64_t *indptr,
+                      int32_t *indices, int32_t *max_indeg, void *ws, size_t ws_bytes, void *stream,
+                      void *counted_event) {
   KNND_CHECK_ARG(friends && indptr && indices, "knnd_csr_build: null pointer");
   KNND_CHECK_ARG(n >= 1 && k >= 1, "knnd_csr_build: bad sizes");
   KNND_CHECK_ARG(n * (int64_t)k < ((int64_t)1 << 31), "knnd_csr_build: n*K must be < 2^31");
@@ -189,6 +195,7 @@ int knnd_csr_build(const int32_t *friends, int64_t n, int32_t k, int64_t row_lo,
   if (max_indeg) KNND_CUDA(cudaMemsetAsync(max_indeg, 0, sizeof(int32_t), st));
   if (m == 0) {
     KNND_CUDA(cudaMemsetAsync(indptr, 0, sizeof(int64_t), st));
+    if (counted_event) KNND_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(counted_event), st));
     return KNND_OK;
   }
   int32_t *cnt = static_cast<int32_t *>(ws);
@@ -205,6 +212,9 @@ int knnd_csr_build(const int32_t *friends, int64_t n, int32_t k, int64_t row_lo,
   }
   csr_reduce_kernel<<<(unsigned)ntiles, SCAN_THREADS, 0, st>>>(cnt, m, tiles, max_indeg);
   KNND_LAUNCHED(1);
+  // max_indeg is final here: a caller that only waits for it (the round's stop test and the
+  // next join's plan) need not wait for the scan and the fill — two thirds of the build
+  if (counted_event) KNND_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(counted_event), st));
   csr_partials_kernel<<<1, SCAN_THREADS, 0, st>>>(tiles, ntiles, indptr, m);
   KNND_LAUNCHED(1);
   csr_apply_kernel<<<(unsigned)ntiles, SCAN_THREADS, 0, st>>>(cnt, m, tiles, indptr);

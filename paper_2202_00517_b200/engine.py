@@ -122,13 +122,17 @@ class CudaOps:
             self._ws[key] = buf
         return buf
 
-    def csr(self, table: torch.Tensor, n: int, k: int, lo: int, hi: int, max_out: torch.Tensor | None) -> Csr:
+    def csr(self, table: torch.Tensor, n: int, k: int, lo: int, hi: int, max_out: torch.Tensor | None,
+            counted: "torch.cuda.Event | None" = None) -> Csr:
+        """`counted` (optional) is recorded on the stream once max_out is final, before
+        the scan and the fill of the build (knnd_csr_build_ev)."""
         indptr = torch.empty(hi - lo + 1, dtype=torch.int64, device=self.device)
         indices = torch.empty(max(n * k, 1), dtype=torch.int32, device=self.device)
         nbytes = _lib.load().knnd_csr_workspace_bytes(n, k, lo, hi)
         ws = self._workspace("csr", nbytes)
-        _lib.call("knnd_csr_build", table.data_ptr(), n, k, lo, hi, indptr.data_ptr(), indices.data_ptr(),
-                  max_out.data_ptr() if max_out is not None else None, ws.data_ptr(), ws.numel(), self._stream())
+        _lib.call("knnd_csr_build_ev", table.data_ptr(), n, k, lo, hi, indptr.data_ptr(), indices.data_ptr(),
+                  max_out.data_ptr() if max_out is not None else None, ws.data_ptr(), ws.numel(), self._stream(),
+                  counted.cuda_event if counted is not None else None)
         return Csr(indptr, indices, lo, hi)
 
     def join(self, tabs, table: torch.Tensor, n: int, k: int, csr: Csr, max_indeg: int, out_rows: torch.Tensor,
@@ -291,6 +295,16 @@ class Engine:
         # [5] this rank's comparisons
         self.stats = torch.zeros(8, dtype=torch.int64, device=device)
         self._stats32 = self.stats.view(torch.int32)
+        # The round's statistics are read behind an event recorded inside the CSR build, as soon
+        # as the max in-degree is final: the host decides (stop test, next plan) and queues the
+        # next round while the build's scan and fill — two thirds of it — still run, so the
+        # device does not idle for the host's latency each round (CUDA ops only).
+        self._stats_ev = self._stats_stream = self._stats_host = None
+        if isinstance(self.ops, CudaOps):
+            self._stats_stream = torch.cuda.Stream(device)
+            self._stats_ev = torch.cuda.Event()
+            self._stats_ev.record(torch.cuda.current_stream(device))  # (creates the CUDA event: its handle is passed on)
+            self._stats_host = torch.zeros(8, dtype=torch.int64).pin_memory()
         # optional CUDA-event bracketing of each local join (bench.py roofline)
         self.join_events: list | None = None
         self.peer: PeerTables | None = None  # fused exchange (P > 1), see enable_peer_exchange
@@ -421,10 +435,18 @@ class Engine:
             else:
                 self.exchange(nxt)
             self.all_reduce(tally)
-        csr_next = self.ops.csr(nxt, self.n, self.k, s.lo, s.hi, self._stats32[9:10])
         if samples is not None:
             self.ops.fcc(nxt, self.n, self.k, samples, self._stats32[8:9])
-        host = self.stats.cpu()  # the one synchronisation of the round
+        if self._stats_ev is not None:
+            csr_next = self.ops.csr(nxt, self.n, self.k, s.lo, s.hi, self._stats32[9:10], counted=self._stats_ev)
+            self._stats_stream.wait_event(self._stats_ev)
+            with torch.cuda.stream(self._stats_stream):
+                self._stats_host.copy_(self.stats, non_blocking=True)
+            self._stats_stream.synchronize()  # the one synchronisation of the round
+            host = self._stats_host.clone()
+        else:
+            csr_next = self.ops.csr(nxt, self.n, self.k, s.lo, s.hi, self._stats32[9:10])
+            host = self.stats.cpu()  # the one synchronisation of the round
         h32 = host.view(torch.int32)
         if ev is not None:
             self.join_events.append((ev[0].elapsed_time(ev[1]), int(host[5])))
