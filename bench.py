@@ -469,7 +469,7 @@ def b200_arm(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": statistics.mean(step_ms), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32 screen + f64 exact rescoring",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32 screen (over %s rows) + f64 exact rescoring" % ("23-bit fixed-point" if gathered != int(tabs.ld) * 4 else "fp32"),
             "data": "synthetic (seeded flat-Dirichlet simplex points, reference generator stream)",
             "config": {"workload": workload_desc(args.config, n, d, k), "n": n, "d": d, "k": k, "seed": seed,
                        "rounds_per_step": rounds, "comparisons_per_step": comps // max(args.steps, 1),

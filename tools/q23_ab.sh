@@ -1,4 +1,3 @@
-./tools/prmt_probe > gpurun_out/prmt_probe.txt 2>&1; cat gpurun_out/prmt_probe.txt
 # A/B of the Q23 screen at C3 (per-class timings + untimed descents), after its parity tests
 timeout 600 python -m pytest tests/test_q23.py -x -q -p no:cacheprovider > gpurun_out/q23_tests.log 2>&1; echo "pytest rc=$?" >> gpurun_out/q23_tests.log
 tail -5 gpurun_out/q23_tests.log
