@@ -364,6 +364,13 @@ def test_c3_trajectory(cuda, trajectories):
 
 
 @pytest.mark.slow
+def test_c3_trajectory_fp32_rows(cuda, trajectories, monkeypatch):
+    """C3 with the fp32 screen rows (KNND_Q23=0): the same per-round tables."""
+    monkeypatch.setenv("KNND_Q23", "0")
+    _trajectory_check(trajectories, "c3")
+
+
+@pytest.mark.slow
 def test_c4_trajectory(cuda, trajectories):
     """n=1M, d=50, K=30: hub anchors (in-degree up to 32,393) exercise every size class."""
     from conftest import load_json

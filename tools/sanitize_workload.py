@@ -83,6 +83,13 @@ def main():
     check_join(6000, 20, 20, [(7, 1500), (11, 600), (13, 800), (17, 160), (19, 60), (23, 40)], peers=True)
     check_join(3000, 8, 64, [(7, 700), (11, 300)])
     check_join(3000, 7, 12, [(5, 900), (9, 200)])
+    check_join(2500, 50, 30, [(3, 800), (8, 250), (21, 90)])  # the 160-byte Q23 rows
+    os.environ["KNND_Q23"] = "0"  # the fp32 screen rows (specialised and generic widths)
+    try:
+        check_join(4000, 20, 20, [(7, 1200), (11, 500), (13, 150), (17, 60)], peers=True)
+        check_join(2000, 6, 10, [(5, 500)])
+    finally:
+        del os.environ["KNND_Q23"]
     # the Euclidean path
     rng = np.random.default_rng(5)
     v = rng.normal(size=(3000, 12))
