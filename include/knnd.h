@@ -14,7 +14,7 @@
  * returns.  The caller (the Python host in
  * paper_2202_00517_b200/, using PyTorch for device buffers) owns all memory.
  * Environment variables read per call (diagnostics / A-B only; results never
- * depend on them): KNND_PLAN, KNND_SIDE_CLASSES, KNND_CLASS_TIMING.
+ * depend on them): KNND_PLAN, KNND_WLIM, KNND_SIDE_CLASSES, KNND_CLASS_TIMING.
  *
  * Return value: KNND_OK (0) or a negative KNND_E* code; knnd_last_error()
  * then describes the failure.  Errors never fall back to a CPU path.
