@@ -773,7 +773,9 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     int Ha = H;
     unsigned sha = shift;
     if constexpr (GTAB) {
-      int la = 15;
+      // (a class table below 2^15 slots arises when small K hands the 2^15 shared-memory
+      // class to this one: then the whole table, which holds 2 Pmax >= 2 total)
+      int la = logH < 15 ? logH : 15;
       while (la < logH && (1 << la) < 2 * total) ++la;
       Ha = 1 << la;
       sha = 32u - (unsigned)la;

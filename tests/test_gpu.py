@@ -363,6 +363,28 @@ def test_c3_trajectory(cuda, trajectories):
     _recall_check("c3", pts, final, load_json("recall.json"), 10_000)
 
 
+@pytest.mark.parametrize("screen", ["q23", "fp32"])
+@pytest.mark.parametrize("n,d,k,copies", [(4400, 6, 2, 920), (10000, 10, 2, 2000), (3000, 8, 3, 1500)])
+def test_small_k_duplicate_hubs_reach_the_global_class(cuda, monkeypatch, n, d, k, copies, screen):
+    """Small K with a block of identical points: every copy ties at distance 0, so the
+    descent concentrates in-degrees of ~`copies` on a few ids; with K = 2 the 2^15-slot
+    shared-memory class cannot stage its S list and hands those anchors to the
+    global-memory class, whose table is then smaller than 2^15 slots (a per-anchor
+    table size assumed at least that: found by tools/fuzz.py, seed 4242)."""
+    monkeypatch.setenv("KNND_Q23", "1" if screen == "q23" else "0")
+    pts = port.experiment_points(n, d, 11).copy()
+    pts[n - copies:] = pts[17]
+    rs = b2.KlRankingSystem(pts, validate=False)
+    tab = native.Tables(pts)
+    cfg = b2.DescentConfig(k=k, seed=5)
+    friends, hist = b2.run(b2.Dataset(pts), rs, cfg)
+    init = native.sort_rows(tab, port.random_kout_draws(n, k, port.substream(5, port.TAG_INIT)))
+    final, ohist = native.descend(tab, init, 5, cfg.fcc_sample_count, cfg.resolved_max_rounds(n))
+    assert [(h.comparisons, h.changed_friend_sets, round(h.fcc * 1000)) for h in hist] == \
+        [(h["comparisons"], h["changed"], h["fcc_count"]) for h in ohist]
+    assert np.array_equal(friends, final)
+
+
 @pytest.mark.slow
 def test_c3_trajectory_fp32_rows(cuda, trajectories, monkeypatch):
     """C3 with the fp32 screen rows (KNND_Q23=0): the same per-round tables."""

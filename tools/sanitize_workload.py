@@ -84,6 +84,7 @@ def main():
     check_join(3000, 8, 64, [(7, 700), (11, 300)])
     check_join(3000, 7, 12, [(5, 900), (9, 200)])
     check_join(2500, 50, 30, [(3, 800), (8, 250), (21, 90)])  # the 160-byte Q23 rows
+    check_join(3000, 7, 2, [(5, 1200), (9, 300)])  # K = 2: the global-memory class with a table below 2^15 slots
     os.environ["KNND_Q23"] = "0"  # the fp32 screen rows (specialised and generic widths)
     try:
         check_join(4000, 20, 20, [(7, 1200), (11, 500), (13, 150), (17, 60)], peers=True)
