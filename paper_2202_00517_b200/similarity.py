@@ -162,7 +162,12 @@ class DeviceTables:
                              device=device)
             _lib.call("knnd_kl_q23_prepare", self.log64.data_ptr(), self.n, self.d, self.q23_bytes,
                       self.q23.data_ptr(), self.qh23.data_ptr(), ws.data_ptr(), ws.numel(), _stream(device))
-            if not bool(torch.isfinite(self.qh23).all().item()):  # (synchronises: ws is a temporary)
+            # (the read synchronises: ws is a temporary.)  A non-finite log, or coordinates so
+            # large (un-normalised data) or steps so small that the screen's fp32 weights
+            # x_j h_j 2^126 would leave the normal range, keep the fp32 rows.
+            hmax = float(self.qh23.max().item())
+            scale = self.max_coord * hmax
+            if not (np.isfinite(hmax) and (hmax == 0.0 or 2.0 ** -100 < scale < 2.0 ** -6)):
                 self.q23 = self.qh23 = None
 
     # -- the kernel calls (one per ABI entry; the L2 tables provide the same methods)

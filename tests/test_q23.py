@@ -115,3 +115,20 @@ def test_q23_size_classes_and_hubs_vs_oracle(cuda, screen):
     assert np.array_equal(uc.cpu().numpy(), o_uc)
     assert np.array_equal(out.cpu().numpy(), o_rows)
     assert tally.cpu().tolist()[:3] == [o_comp, o_changed, 0]
+
+
+def test_q23_unnormalised_scales_keep_fp32_rows(cuda, q23_on):
+    """The screen's fp32 weights x_j h_j 2^126 must stay in the normal range: KL data far
+    from the simplex (validate=False) screen the fp32 rows, and a round still equals the oracle's."""
+    base = port.experiment_points(1500, 8, 4)
+    for scale, q23 in ((1.0, True), (3.0, True), (1e7, False)):
+        pts = base * scale
+        rs = b2.KlRankingSystem(pts, validate=False)
+        assert (rs.device_tables().q23 is not None) == q23, scale
+        k = 10
+        tab = native.Tables(pts)
+        init = native.sort_rows(tab, port.random_kout_draws(1500, k, port.substream(3, port.TAG_INIT)))
+        nxt, s = b2.run_round(b2.KnnState(init), rs, b2.DescentConfig(k=k, seed=3))
+        rows, _, _, comps, changed = native.local_join(tab, init)
+        assert np.array_equal(nxt.friends, rows), scale
+        assert (s.comparisons, s.changed_friend_sets) == (comps, changed)
