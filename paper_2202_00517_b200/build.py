@@ -23,8 +23,9 @@ LIB_PATH = os.path.join(PKG_DIR, "libknnd.so")
 CHECKED_LIB_PATH = os.path.join(PKG_DIR, "libknnd_checked.so")
 OBJ_DIR = os.path.join(PKG_DIR, "_obj")
 
-SOURCES = ["abi.cu", "prep.cu", "csr.cu", "join.cu", "rng.cu", "exact.cu"]
-HEADERS = ["common.cuh", "score.cuh"]
+# (the join's kernel families are three translation units so that they compile in parallel)
+SOURCES = ["abi.cu", "prep.cu", "csr.cu", "join.cu", "join_f32k2.cu", "join_q23.cu", "rng.cu", "exact.cu"]
+HEADERS = ["common.cuh", "score.cuh", "join_impl.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + [
@@ -75,8 +76,8 @@ def build(force: bool = False, verbose: bool = False, checked: bool = True) -> s
         return obj, res.stderr
 
     jobs = [(src, obj_dir, extra) for _, obj_dir, extra in targets for src in SOURCES]
-    # the largest translation units first (join.cu dominates the build)
-    jobs.sort(key=lambda j: -os.path.getsize(os.path.join(CSRC, j[0])))
+    # the join's translation units first (their template instantiations dominate the build), then by size
+    jobs.sort(key=lambda j: (not j[0].startswith("join"), -os.path.getsize(os.path.join(CSRC, j[0]))))
     with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as pool:
         results = dict(zip(jobs, pool.map(compile_one, jobs)))
     for lib_path, obj_dir, extra in targets:

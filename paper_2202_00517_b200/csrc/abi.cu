@@ -96,7 +96,8 @@ int knnd_check_failures(unsigned long long *count, unsigned long long *first) {
   *first = 0;
 #ifdef KNND_CHECKED
   int rc = KNND_OK;
-  if ((rc = knnd::check_read_abi(count, first)) || (rc = knnd::check_read_join(count, first)) || (rc = knnd::check_read_exact(count, first)) ||
+  if ((rc = knnd::check_read_abi(count, first)) || (rc = knnd::check_read_join(count, first)) ||
+      (rc = knnd::check_read_join_f32k2(count, first)) || (rc = knnd::check_read_join_q23(count, first)) || (rc = knnd::check_read_exact(count, first)) ||
       (rc = knnd::check_read_csr(count, first)) || (rc = knnd::check_read_prep(count, first)) ||
       (rc = knnd::check_read_rng(count, first))) {
     knnd::set_error("knnd_check_failures: reading the check words failed");

@@ -84,6 +84,8 @@ static __device__ unsigned long long g_check[2];  // [0] failures, [1] first fai
   }
 int check_read_abi(unsigned long long *, unsigned long long *);
 int check_read_join(unsigned long long *, unsigned long long *);
+int check_read_join_f32k2(unsigned long long *, unsigned long long *);
+int check_read_join_q23(unsigned long long *, unsigned long long *);
 int check_read_exact(unsigned long long *, unsigned long long *);
 int check_read_csr(unsigned long long *, unsigned long long *);
 int check_read_prep(unsigned long long *, unsigned long long *);

@@ -1,0 +1,13 @@
+// The local join's Q23-row kernel family, KL and Euclidean (join_impl.cuh; host side in join.cu).
+#include "join_impl.cuh"
+
+namespace knnd {
+
+int join_dispatch_q23(const Plan &P, int i, const JoinParams &p, const int32_t *lists, const int32_t *counts,
+                      int64_t m, int32_t *slabs, cudaStream_t st) {
+  return dispatch_class_family<FAM_Q23>(P, i, p, lists, counts, m, slabs, st);
+}
+
+}  // namespace knnd
+
+KNND_CHECK_READER(join_q23, 8)

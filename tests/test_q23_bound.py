@@ -1,5 +1,5 @@
 """The Q23 screen's error model, checked on the host: a numpy emulation of
-knnd_kl_q23_prepare (prep.cu) and of screen_row_q23 / q23_weights (join.cu) —
+knnd_kl_q23_prepare (prep.cu) and of screen_row_q23 / q23_weights (join_impl.cuh) —
 the same quantisation, the same fp32 weights, the same four FMA chains — must
 stay within the bound the join's thresholds and certification rely on:
 
