@@ -8,8 +8,11 @@ events one shard at a time — and the per-round critical path is the slowest
 shard's CSR + join, plus the replicated FCC.  The exchange is the fused peer
 store (overlapped with the join) and a device barrier + 32-byte all-reduce,
 added as a fixed per-round cost (`--sync-us`, default 30 us), and every P
-pays the per-round host cost (`--host-us`, default 80 us, tools/round_overhead.py).  Prints one
-JSON line per P with the projected descent time and speed-up over P = 1.
+pays the per-round host cost (`--host-us`, default 80 us, tools/round_overhead.py) less the part
+of it that overlaps the CSR build's tail: the round's statistics are read behind an event recorded
+inside the build (knnd_csr_build_ev), so only max(0, host - tail) is exposed, the tail (scan + fill)
+being timed per shard.  Prints one JSON line per P with the projected descent time and speed-up
+over P = 1.
 
 Usage: python tools/shard_projection.py [n d k] [--sync-us 30]
 """
@@ -57,12 +60,20 @@ def timed(fn):
 def shard_costs(state, P, samples):
     """(max over ranks of CSR ms, max over ranks of join ms, fcc ms) for one round input."""
     eng = state._engine
-    csr_ms, join_ms = [], []
+    csr_ms, join_ms, tails = [], [], []
     for r in range(P):
         s = Shard(r, P, n)
         mx = torch.zeros(2, dtype=torch.int32, device=dev)
         eng.ops.csr(state._table, n, k, s.lo, s.hi, mx[0:1])  # warm (workspace, first launch)
         t_csr = min(timed(lambda: eng.ops.csr(state._table, n, k, s.lo, s.hi, mx[0:1]))[0] for _ in range(3))
+        # the part of the build after the event the statistics wait for (scan + fill)
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        e1 = torch.cuda.Event(enable_timing=True)
+        eng.ops.csr(state._table, n, k, s.lo, s.hi, mx[0:1], counted=ev)
+        e1.record()
+        torch.cuda.synchronize()
+        tails.append(ev.elapsed_time(e1))
         csr = eng.ops.csr(state._table, n, k, s.lo, s.hi, mx[0:1])
         max_indeg = int(mx[0].item())
         out = torch.empty((s.hi - s.lo, k), dtype=torch.int32, device=dev)
@@ -77,7 +88,7 @@ def shard_costs(state, P, samples):
     cnt = torch.zeros(1, dtype=torch.int32, device=dev)
     eng.ops.fcc(state._table, n, k, samples, cnt)
     t_fcc, _ = timed(lambda: eng.ops.fcc(state._table, n, k, samples, cnt))
-    return max(csr_ms), max(join_ms), t_fcc, join_ms
+    return max(csr_ms), max(join_ms), t_fcc, join_ms, min(tails)
 
 
 st = b2.init_random_kout(b2.Dataset(pts), rs, cfg, b2.derive_rng(0, 2))
@@ -88,13 +99,14 @@ from paper_2202_00517_b200.descent import draw_fcc_schedule, _to_device  # noqa:
 smp = _to_device(draw_fcc_schedule(n, k, cfg, cfg.resolved_max_rounds(n)), dev)
 for r in range(1, cfg.resolved_max_rounds(n) + 1):
     for P in P_LIST:
-        c, j, f, js = shard_costs(st, P, smp[r - 1])
+        c, j, f, js, tail = shard_costs(st, P, smp[r - 1])
         acc = per_p[P]
         acc["csr"] += c
         acc["join"] += j
         acc["fcc"] += f
-        acc["sync"] += (args.sync_us / 1e3 if P > 1 else 0.0) + args.host_us / 1e3
-        acc["rounds"].append({"round": r, "join_ms_per_rank": [round(x, 3) for x in js], "csr_ms": round(c, 3)})
+        acc["sync"] += (args.sync_us / 1e3 if P > 1 else 0.0) + max(0.0, args.host_us / 1e3 - tail)
+        acc["rounds"].append({"round": r, "join_ms_per_rank": [round(x, 3) for x in js], "csr_ms": round(c, 3),
+                              "csr_tail_ms": round(tail, 3)})
     st, s = b2.run_round(st, rs, cfg)
     hist.append(s)
     if len(hist) >= 2 and hist[-1].fcc <= hist[-2].fcc:
