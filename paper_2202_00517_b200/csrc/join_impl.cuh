@@ -935,13 +935,7 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
     float best0 = mn, best1 = mn;  // this lane's two smallest screened values
     float4 xreg[NV4 > 0 && !Q23S ? NV4 : 1];  // the anchor's fp32 row in registers
     float wq[Q23<Q23S ? NV4 : 1>::NQ];  // Q23: the anchor's weights
-    if constexpr (Q23S) {
-      // the quantisation part of the bound, per anchor (+ the Euclidean scorer's fp64 term in these units)
-      if constexpr (Q23SIGNED)
-        slack = q23_weights_signed<NV4>(x32, p.qh, p.d64, wq, abq) + p.slack * 0x1p-23f;
-      else
-        slack = q23_weights<NV4>(x64, p.qh, d, wq);
-    } else if constexpr (NV4 > 0) {
+    if constexpr (!Q23S && NV4 > 0) {
 #pragma unroll
       for (int q = 0; q < NV4; ++q) xreg[q] = reinterpret_cast<const float4 *>(x32)[q];
     }
@@ -958,6 +952,14 @@ __global__ void __launch_bounds__(G) join_kernel(JoinParams p, const int32_t *__
         else
           stage_rows_f32<NV4>(wstage, p.log32, list + k0, min(wrows, U - k0), ld, lane);
         cp_async_commit();
+      }
+      if constexpr (Q23S) {
+        // the anchor's weights, computed while the first batch is in flight; the return value is
+        // the quantisation part of the bound, per anchor (+ the Euclidean scorer's fp64 term)
+        if constexpr (Q23SIGNED)
+          slack = q23_weights_signed<NV4>(x32, p.qh, p.d64, wq, abq) + p.slack * 0x1p-23f;
+        else
+          slack = q23_weights<NV4>(x64, p.qh, d, wq);
       }
       for (int buf = 0; k0 < U; k0 += kstep, buf ^= 1) {
         const int nrow = min(wrows, U - k0);
@@ -1295,13 +1297,7 @@ __global__ void __launch_bounds__(128, 4)
     float4 xreg[NV4 > 0 && !Q23S ? NV4 : 1];  // the anchor's fp32 row in registers
     float wq[Q23<Q23S ? NV4 : 1>::NQ];  // Q23: the anchor's weights
     float slack = p.slack, abq = 0.f;           // the absolute part of the fp32 / Q23 bound (abq: Euclidean Q23)
-    if constexpr (Q23S) {
-      // the quantisation part of the bound, per anchor (+ the Euclidean scorer's fp64 term in these units)
-      if constexpr (Q23SIGNED)
-        slack = q23_weights_signed<NV4>(x32, p.qh, p.d64, wq, abq) + p.slack * 0x1p-23f;
-      else
-        slack = q23_weights<NV4>(x64, p.qh, d, wq);
-    } else if constexpr (NV4 > 0) {
+    if constexpr (!Q23S && NV4 > 0) {
 #pragma unroll
       for (int q = 0; q < NV4; ++q) xreg[q] = reinterpret_cast<const float4 *>(x32)[q];
     }
@@ -1436,6 +1432,16 @@ __global__ void __launch_bounds__(128, 4)
       else
         stage_rows_f32<NV4>(stage, p.log32, list, min(rows, U), ld, lane);
       cp_async_commit();
+    }
+    if constexpr (Q23S) {
+      // The anchor's weights, computed while the first batch is in flight — and not before
+      // the dedup, where they would hold NQ registers through it.  The return value is the
+      // quantisation part of the bound, per anchor (+ the Euclidean scorer's fp64 term in
+      // these units).
+      if constexpr (Q23SIGNED)
+        slack = q23_weights_signed<NV4>(x32, p.qh, p.d64, wq, abq) + p.slack * 0x1p-23f;
+      else
+        slack = q23_weights<NV4>(x64, p.qh, d, wq);
     }
     for (int k0 = 0, buf = 0; k0 < U; k0 += rows, buf ^= 1) {
       const int nrow = min(rows, U - k0);
