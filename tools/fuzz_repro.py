@@ -55,6 +55,18 @@ for rnd in range(1, 12):
         print("  max indeg", indeg.max(), "anchors with wrong |U|:", wrongu.size, [(int(x), int(indeg[x]), int(ucd[x]), int(uc[x])) for x in wrongu[:8]])
         P = (k + indeg) * (k + 1)
         print("  P of wrong-row anchors", [int(P[x]) for x in bad[:8]], " P of wrong-|U| anchors", sorted(set(int(P[x]) for x in wrongu))[:10])
+        # a differing row is within the parity contract when it is a reordering of candidates
+        # whose fp64 scores tie within 1e-6 relative of the cross entropy (the reference's
+        # einsum and the device's FMA chain round differently at ~1e-16)
+        ties = 0
+        for x in bad:
+            if sorted(got[x]) == sorted(rows[x]):
+                sc = rs.batch_scores(int(x), rows[x].astype(np.int64))
+                ce = float(-(pts[x] * np.log(pts[rows[x][0]])).sum())
+                pos = [i for i in range(k) if got[x][i] != rows[x][i]]
+                if np.ptp(sc[pos]) <= 1e-6 * max(abs(ce), 1e-300):
+                    ties += 1
+        print(f"  differing rows that only reorder ties within 1e-6 relative: {ties} of {bad.size}")
         for x in bad[:6]:
             print("  anchor", x, "indeg", indeg[x], "|U|", uc[x], "got", got[x], "want", rows[x],
                   "kl got", [float(rs.batch_scores(int(x), np.array([g]))[0]) for g in got[x]],
